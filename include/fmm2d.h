@@ -1,0 +1,132 @@
+/* fmm2d.h -- C ABI of the B200-native adaptive 2-D FMM (libfmm2d.so).
+ *
+ * The reference package (/root/reference/pkg, python `fmm2d` 0.1.0) has no
+ * FFI; its drop-in boundary is the Python call
+ *     fmm_evaluate(points: ParticleSet, cfg: TreeConfig, *, parallel, n_workers)
+ *         -> (values complex128[M] in input order, EngineReport)
+ * (pkg/src/fmm2d/engine.py:207-279).  Each entry point below replaces one
+ * reference interface; the Python host package `paper_1205_4611_b200` binds
+ * them with ctypes and keeps the reference's Python signatures (see
+ * INTEGRATION.md for the binding a maintainer of the reference would add).
+ *
+ * Conventions: complex arrays are interleaved (re, im) doubles, i.e. the
+ * memory of a numpy complex128 array.  Host pointers unless the function name
+ * says `_device`.  The library never frees caller memory.  A context is not
+ * thread-safe; one in-flight call per context.  Every call is synchronous.
+ * Return codes map to the reference's exception types:
+ *   FMM2D_EBADARG -> ValueError, FMM2D_EDEGENERATE -> DegenerateInputError
+ *   (tree.py:83-84), FMM2D_ESINGULAR -> ValueError with the reference message,
+ *   FMM2D_ECUDA / FMM2D_ENCCL -> RuntimeError, FMM2D_EOOM -> MemoryError.
+ * fmm2d_last_error() returns the message (same text as the reference raises).
+ */
+#ifndef FMM2D_H
+#define FMM2D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMM2D_OK 0
+#define FMM2D_EBADARG 2
+#define FMM2D_EDEGENERATE 3
+#define FMM2D_ESINGULAR 5
+#define FMM2D_ECUDA 6
+#define FMM2D_ENCCL 7
+#define FMM2D_EOOM 8
+
+#define FMM2D_NPHASES 9 /* engine.py:28 PHASE_NAMES order:
+                           sort connect p2m m2m m2l l2l l2p p2p other */
+
+typedef struct fmm2d_ctx fmm2d_ctx;
+
+/* EngineReport (engine.py:34-47) plus device-side extras */
+typedef struct fmm2d_report {
+  double phase_ms[FMM2D_NPHASES]; /* CUDA-event time per phase; other = copies */
+  double device_ms;               /* first tree kernel .. last P2P kernel */
+  double total_ms;                /* whole call incl. H2D/D2H */
+  int32_t n_levels;
+  int32_t retries;                /* list-capacity regrow reruns */
+  int64_t n_boxes;
+  int64_t finest_src_min;
+  int64_t finest_src_max;
+  double finest_src_mean;
+  int64_t p2p_skips;              /* raw coincident pairs skipped (self included) */
+  int64_t list_totals[4];         /* weak, p2p, p2l, m2p entries */
+  int32_t max_len[4];             /* longest list of each kind */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} fmm2d_report;
+
+/* context on CUDA device `device` (buffers, stream, events grow monotonically) */
+int fmm2d_create(fmm2d_ctx** out, int device);
+void fmm2d_destroy(fmm2d_ctx* ctx);
+const char* fmm2d_last_error(const fmm2d_ctx* ctx);
+
+/* tree.py:149-157 num_levels + tree.py:249-255 clamp (4^L <= n) */
+int fmm2d_num_levels(int64_t n_sources, int n_desired);
+/* tree.py:149-157 unclamped Eq. (6); -1 on bad input */
+int fmm2d_num_levels_raw(int64_t n_sources, int n_desired);
+
+/* replaces fmm2d.engine.fmm_evaluate (engine.py:207-279).
+ * pos_xy: c128[n]; gamma: f64[n]; eval_xy: c128[m] or NULL (evaluation points
+ * alias the sources, m must equal n); out_xy: c128[m] in input order. */
+int fmm2d_evaluate(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
+                   int64_t m, const double* eval_xy, int p, double theta, int n_desired,
+                   double* out_xy, fmm2d_report* rep);
+
+/* same pipeline with inputs/outputs already resident in device memory of the
+ * context's device (used by the bench's device-resident measurement) */
+int fmm2d_evaluate_device(fmm2d_ctx* ctx, int64_t n, const double* d_pos_xy,
+                          const double* d_gamma, int64_t m, const double* d_eval_xy, int p,
+                          double theta, int n_desired, double* d_out_xy, fmm2d_report* rep);
+
+/* replaces fmm2d.tree.build_tree (tree.py:293-397): builds on the device and
+ * keeps the tree in the context; fetch it with fmm2d_export_tree */
+int fmm2d_build_tree(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
+                     int64_t m, const double* eval_xy, int n_desired, int32_t* n_levels);
+
+/* after FMM2D_EDEGENERATE: info = {points in box, box, level, levels still
+ * required}, xy = the common coordinate (tree.py:348-354 message fields) */
+int fmm2d_degenerate_info(fmm2d_ctx* ctx, int64_t info[4], double xy[2]);
+
+/* copy the context's current tree (after build_tree or evaluate).  Level
+ * arrays are concatenated over levels 0..L: boxes ((4^l-1)/3 + k), offsets
+ * (sum_{l'<l}(4^l'+1) + k).  Any output pointer may be NULL. */
+int fmm2d_export_tree(fmm2d_ctx* ctx, double* center_xy, double* half_width, double* half_height,
+                      int64_t* src_offsets, int64_t* eval_offsets, int64_t* src_perm,
+                      int64_t* eval_perm, double* src_pos_xy, double* src_strength,
+                      double* eval_pos_xy);
+
+/* replaces fmm2d.connectivity.build_connectivity (connectivity.py:99-114)
+ * for a tree given by its per-level geometry (concatenated as above) */
+int fmm2d_build_connectivity(fmm2d_ctx* ctx, int n_levels, const double* center_xy,
+                             const double* half_width, const double* half_height, double theta);
+
+/* totals of the context's current lists: weak (all levels), p2p, p2l, m2p */
+int fmm2d_list_sizes(fmm2d_ctx* ctx, int64_t totals[4]);
+
+/* CSR copies; weak_* over all boxes of all levels (global box ids as above),
+ * p2p/p2l/m2p over finest boxes (finest-level ids). */
+int fmm2d_export_lists(fmm2d_ctx* ctx, int64_t* weak_off, int64_t* weak_idx, int64_t* p2p_off,
+                       int64_t* p2p_idx, int64_t* p2l_off, int64_t* p2l_idx, int64_t* m2p_off,
+                       int64_t* m2p_idx);
+
+/* list-length histogram of the last evaluate: kind 0 weak, 1 p2p, 2 p2l, 3 m2p;
+ * out[len] = number of lists of that length for len < nbins */
+int fmm2d_histogram(fmm2d_ctx* ctx, int kind, int64_t* out, int nbins);
+
+/* debug seams for per-phase parity: expansions of the last evaluate
+ * (c128[n_boxes * (p+1)], global box ids) and tree-ordered potentials */
+int fmm2d_export_expansions(fmm2d_ctx* ctx, double* mult_xy, double* local_xy);
+int fmm2d_export_phi(fmm2d_ctx* ctx, double* phi_xy);
+
+/* replaces fmm2d.engine.direct_evaluate (engine.py:282-300), asymmetric mode */
+int fmm2d_direct(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
+                 int64_t m, const double* eval_xy, double* out_xy);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM2D_H */

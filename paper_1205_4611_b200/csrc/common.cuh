@@ -1,0 +1,135 @@
+// Shared device helpers for the B200 FMM engine (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef __CUDA_ARCH__
+#define FMM_HD
+#else
+#define FMM_HD
+#endif
+
+namespace fmm {
+
+// ----------------------------------------------------------------------------
+// status word shared by every kernel (device memory, copied back once per call)
+enum : int {
+  ST_OK = 0,
+  ST_DEGENERATE = 1,      // tree.py:348-354
+  ST_P2L_SINGULAR = 2,    // operators.py:216-217
+  ST_M2L_SINGULAR = 4,    // operators.py:329-330
+  ST_M2P_SINGULAR = 8,    // operators.py:376-377
+  ST_OVERFLOW = 16,       // a list buffer was too small: host regrows + reruns
+};
+
+struct DevStatus {
+  int flags;                              // OR of ST_* bits
+  int pad0;
+  unsigned long long degenerate_key;      // (level << 40) | box ; min wins
+  unsigned long long p2p_skips;           // coincident pairs skipped in P2P
+  long long need_weak;                    // required capacities on overflow
+  long long need_strong;
+  long long need_p2p;
+  long long need_p2l;
+  long long need_m2p;
+  int max_len[4];                         // weak, p2p, p2l, m2p list lengths
+  int overflow_where;
+  int pad1;
+};
+
+// ----------------------------------------------------------------------------
+// complex double in registers
+struct cplx {
+  double x, y;
+};
+
+__device__ __forceinline__ cplx cmk(double x, double y) { return cplx{x, y}; }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cplx{fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+__device__ __forceinline__ cplx cscale(cplx a, double s) { return cplx{a.x * s, a.y * s}; }
+// 1/z in real arithmetic (conjugate over squared modulus); caller guarantees z != 0
+__device__ __forceinline__ cplx crcp(cplx z) {
+  double s = 1.0 / fma(z.x, z.x, z.y * z.y);
+  return cplx{z.x * s, -z.y * s};
+}
+
+// ----------------------------------------------------------------------------
+// Bit-exact restatements of the two magnitude algorithms the reference's
+// θ-criterion runs through (pinned against numpy by tests/test_predicates.py
+// via oracle/predicates.c, which holds the same formulas for gcc).
+//
+// radius: np.hypot -> glibc 2.39 __hypot, non-FMA kernel (geometry.py:27-29)
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    double d = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, d), ax));
+    t2 = __dmul_rn(__dsub_rn(d, __dmul_rn(2.0, __dsub_rn(ax, ay))), d);
+  } else {
+    double d = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, d), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, d), ay), ay), __dmul_rn(d, d));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+
+__device__ __forceinline__ double glibc_hypot(double x, double y) {
+  const double SCALE = 0x1p-600, LARGE = 0x1p+511, TINY = 0x1p-511, EPS = 0x1p-54;
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  if (ax > LARGE) {
+    if (ay <= __dmul_rn(ax, EPS)) return __dadd_rn(ax, ay);
+    return __ddiv_rn(glibc_hypot_kernel(__dmul_rn(ax, SCALE), __dmul_rn(ay, SCALE)), SCALE);
+  }
+  if (ay < TINY) {
+    if (ax >= __ddiv_rn(ay, EPS)) return __dadd_rn(ax, ay);
+    return __dmul_rn(glibc_hypot_kernel(__ddiv_rn(ax, SCALE), __ddiv_rn(ay, SCALE)), SCALE);
+  }
+  if (ay <= __dmul_rn(ax, EPS)) return __dadd_rn(ax, ay);
+  return glibc_hypot_kernel(ax, ay);
+}
+
+// distance: np.abs(complex) -> numpy SIMD cabs on FMA hosts (geometry.py:40,53)
+__device__ __forceinline__ double numpy_cabs(double dx, double dy) {
+  double ax = fabs(dx), ay = fabs(dy);
+  double l = ax < ay ? ay : ax;
+  double s = ax < ay ? ax : ay;
+  if (l == 0.0) return 0.0;
+  double q = __ddiv_rn(s, l);
+  return __dmul_rn(l, __dsqrt_rn(__fma_rn(q, q, 1.0)));
+}
+
+// θ-criterion, geometry.py:41 (normal) / :54 (swapped); no contraction
+__device__ __forceinline__ bool well_separated(double ra, double rb, double d, double theta) {
+  double big = fmax(ra, rb), small = fmin(ra, rb);
+  return __dadd_rn(big, __dmul_rn(theta, small)) <= __dmul_rn(theta, d);
+}
+__device__ __forceinline__ bool well_separated_swapped(double ra, double rb, double d,
+                                                       double theta) {
+  double big = fmax(ra, rb), small = fmin(ra, rb);
+  return __dadd_rn(small, __dmul_rn(theta, big)) <= __dmul_rn(theta, d);
+}
+
+// ----------------------------------------------------------------------------
+// order-preserving 64-bit key of a double (-0.0 folded onto +0.0)
+__device__ __forceinline__ unsigned long long ordered_key(double v) {
+  if (v == 0.0) v = 0.0;
+  unsigned long long b = __double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// ----------------------------------------------------------------------------
+// warp helpers
+__device__ __forceinline__ double shfl_down_d(double v, int d) {
+  return __shfl_down_sync(0xffffffffu, v, d);
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace fmm

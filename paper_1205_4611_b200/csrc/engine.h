@@ -1,0 +1,127 @@
+// Host-side declarations shared by the engine translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fmm {
+
+#define FMM_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) throw CudaError(e_, #call, __FILE__, __LINE__);          \
+  } while (0)
+
+struct CudaError {
+  cudaError_t err;
+  std::string what;
+  CudaError(cudaError_t e, const char* call, const char* file, int line);
+};
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void reserve(size_t nbytes);
+  template <class T> T* as() const { return static_cast<T*>(p); }
+  ~DBuf();
+};
+
+// per (N, M, L) plan: data-independent segment offsets and partition tiles
+struct TreePlan {
+  int64_t n = -1, m = -1;
+  int L = -1, S = 0, sb = 0;
+  int smem_bytes = 0;
+  bool global_leaf_finalize = false;
+  std::vector<int> tile_base;        // per global step s < sb: first tile index
+  std::vector<int> tile_count;       // per global step
+  DBuf d_off;                        // int32 offsets for steps 0..S (+1 per step)
+  DBuf d_tile_seg, d_tile_start;     // concatenated tile tables of all global steps
+};
+
+__host__ __device__ inline int64_t step_base(int s) { return (int64_t(1) << s) - 1; }          // per-segment tables
+__host__ __device__ inline int64_t off_base(int s) { return (int64_t(1) << s) - 1 + s; }        // offset tables (+1 each)
+__host__ __device__ inline int64_t level_base(int l) { return ((int64_t(1) << (2 * l)) - 1) / 3; }  // boxes above level l
+
+// device state of one tree (kept between phases of an evaluation)
+struct TreeState {
+  int64_t n = 0, m = 0;
+  int L = 0;
+  bool aliased = true;
+  DBuf pos, g, epos;                 // owned input copies, original order
+  const double2* pos_p = nullptr;    // inputs actually used (owned copies or caller's
+  const double* g_p = nullptr;       //   device memory), original order
+  const double2* epos_p = nullptr;
+  DBuf keys_in, keys_out, vals_in, vals_out, cub_tmp;
+  DBuf xs_sorted, ys_sorted, perm_x, perm_y, rank_x, rank_y;
+  DBuf X0, X1, Y0, Y1;               // int2 (rank_x, rank_y) arrays
+  DBuf xpar0, xpar1, ypar0, ypar1, cutrank;
+  DBuf tile_cnt, tile_pre;
+  DBuf rect_tab, cut_tab, axis_tab;
+  DBuf leaf_of;                      // eval/source leaf ids (fallback + evals)
+  // outputs (tree order)
+  DBuf src_pos, src_g, src_perm;     // double2, double, int32
+  DBuf eval_pos, eval_perm;          // double2, int32
+  DBuf eval_leaf_off;                // int32[4^L + 1]
+  DBuf box_cx, box_cy, box_hw, box_hh, box_r;  // all levels, global box id
+  DBuf bbox;                         // double[4] + scratch
+};
+
+struct ListState {
+  long long cap_weak = 0, cap_strong = 0, cap_p2p = 0, cap_p2l = 0, cap_m2p = 0;
+  DBuf weak_off;                     // int32[nboxes_total + 1] global CSR
+  DBuf weak_idx, weak_tgt;           // int32 (source global id, target global id)
+  DBuf s_off[2], s_idx[2];           // strong lists ping-pong (level-local ids)
+  DBuf cnt_a, cnt_b, cnt_c;          // per-target counts
+  DBuf p2p_off, p2p_idx, p2l_off, p2l_idx, m2p_off, m2p_idx;  // finest, level-local ids
+  DBuf totals;                       // int64 scratch for scans
+  DBuf hist;                         // int32 histograms [4][HIST_BINS]
+};
+
+constexpr int HIST_BINS = 4096;
+
+struct ExpState {
+  int p = 0;
+  DBuf mult, local;                  // double2[nboxes_total * (p+1)]
+  DBuf phi;                          // double2[M] tree order
+  DBuf values;                       // double2[M] input order
+  DBuf partials, item_flags;         // M2L cross-warp partial sums
+};
+
+// ---------------------------------------------------------------------------
+// launchers (all enqueue on `st`, no host sync)
+int plan_levels(int64_t n, int nd);
+void plan_tree(TreePlan& plan, int64_t n, int64_t m, int L);
+void run_tree(TreeState& T, TreePlan& plan, DevStatus* dstat, cudaStream_t st);
+
+void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus* dstat,
+                      cudaStream_t st);
+
+void compute_radius(TreeState& T, cudaStream_t st);
+void run_upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
+                DevStatus* dstat, cudaStream_t st);
+void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st);
+void run_m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
+             cudaStream_t st);
+void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st);
+void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
+                 cudaStream_t st);
+void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
+             double2* values, DevStatus* dstat, cudaStream_t st);
+void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st);
+
+void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
+                double2* out, cudaStream_t st);
+
+// device-wide exclusive scan of int32 counts: out[i] = *base + sum(in[0..i)),
+// out[n] = *base + total (base = 0 when null).  `tmp` is grown as needed.
+void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t st,
+                    const int* base = nullptr);
+
+bool p_supported(int p);
+
+}  // namespace fmm

@@ -1,0 +1,784 @@
+// Tree build ("sort" phase): the asymmetric-adaptive pyramid of successive
+// median splits, bit-exact with the reference's canonical form.
+//
+// Reference: tree.py:293-397 (build_tree), :160-177 (partition_median),
+// :258-285 (_split_sources/_split_evals/_cut_rect), geometry.py:57-63.
+//
+// Design (B200): instead of a k-th-element selection per box per split step,
+// every source gets its global rank along x and along y once (two 64-bit key
+// radix sorts, ties by index).  Each split segment is kept twice, ordered by
+// x-rank and by y-rank.  Splitting a segment along x is then free in the
+// x-ordered copy (left = first k) and a stable partition "rank_x <= cut rank"
+// in the y-ordered copy -- so every step moves one 8-byte (rank_x, rank_y)
+// record per source and never selects.  Because every partition is stable
+// from the identity order, each segment's members are always in ascending
+// original index, which is exactly the canonical tree.  Top steps (large
+// segments) run as tiled global partitions; once a segment fits in shared
+// memory one CTA finishes its whole subtree in SMEM.  Evaluation points do
+// not influence the cuts: each one descends the finished cut table
+// (`coord <= cut`, tree.py:273) to its leaf, then a stable radix sort by leaf
+// yields eval_perm.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "engine.h"
+
+namespace fmm {
+
+namespace {
+
+constexpr int PART_THREADS = 256;
+constexpr int PART_ITEMS = 8;
+constexpr int PART_TILE = PART_THREADS * PART_ITEMS;
+constexpr int SUB_THREADS = 512;
+constexpr int SMEM_BUDGET = 110 * 1024;   // two subtree CTAs per SM
+constexpr int LEAF_SMEM_MAX = 512;        // in-SMEM index sort of leaves up to this size
+
+struct Rect {
+  double x0, x1, y0, y1;
+};
+
+// --------------------------------------------------------------------------
+// bounding box of sources and evaluation points (tree.py:319-322)
+__global__ void k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__ epos,
+                       long long m, double* out, unsigned int* counter, double* partial) {
+  double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n + m;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 z = i < n ? pos[i] : epos[i - n];
+    x0 = fmin(x0, z.x); x1 = fmax(x1, z.x);
+    y0 = fmin(y0, z.y); y1 = fmax(y1, z.y);
+  }
+  for (int d = 16; d; d >>= 1) {
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, d));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, d));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, d));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, d));
+  }
+  __shared__ double sw[4][32];
+  __shared__ bool last;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sw[0][w] = x0; sw[1][w] = x1; sw[2][w] = y0; sw[3][w] = y1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)blockDim.x / 32; ++q) {
+      x0 = fmin(x0, sw[0][q]); x1 = fmax(x1, sw[1][q]);
+      y0 = fmin(y0, sw[2][q]); y1 = fmax(y1, sw[3][q]);
+    }
+    partial[4 * blockIdx.x + 0] = x0; partial[4 * blockIdx.x + 1] = x1;
+    partial[4 * blockIdx.x + 2] = y0; partial[4 * blockIdx.x + 3] = y1;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      x0 = fmin(x0, partial[4 * q + 0]); x1 = fmax(x1, partial[4 * q + 1]);
+      y0 = fmin(y0, partial[4 * q + 2]); y1 = fmax(y1, partial[4 * q + 3]);
+    }
+    out[0] = x0; out[1] = x1; out[2] = y0; out[3] = y1;
+    *counter = 0;
+  }
+}
+
+__global__ void k_root_rect(const double* bbox, Rect* rect_tab) {
+  rect_tab[0] = Rect{bbox[0], bbox[1], bbox[2], bbox[3]};
+}
+
+// --------------------------------------------------------------------------
+// rank keys
+__global__ void k_make_keys(const double2* __restrict__ pos, long long n, int axis,
+                            unsigned long long* keys, int* vals) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 z = pos[i];
+  keys[i] = ordered_key(axis ? z.y : z.x);
+  vals[i] = (int)i;
+}
+
+__global__ void k_rank_scatter(const double2* __restrict__ pos, long long n, int axis,
+                               const int* __restrict__ perm, double* sorted, int* rank) {
+  long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int i = perm[r];
+  double2 z = pos[i];
+  sorted[r] = axis ? z.y : z.x;
+  rank[i] = (int)r;
+}
+
+__global__ void k_init_arrays(long long n, const int* __restrict__ perm_x,
+                              const int* __restrict__ perm_y, const int* __restrict__ rank_x,
+                              const int* __restrict__ rank_y, int2* X, int2* Y,
+                              unsigned char* xpar, unsigned char* ypar) {
+  long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r == 0) { xpar[0] = 0; ypar[0] = 0; }
+  if (r >= n) return;
+  X[r] = make_int2((int)r, rank_y[perm_x[r]]);
+  Y[r] = make_int2(rank_x[perm_y[r]], (int)r);
+}
+
+// --------------------------------------------------------------------------
+// one split step, per segment: axis, cut, child rectangles, degenerate check
+struct StepArgs {
+  const int* off;           // step offsets table
+  Rect* rect_tab;
+  double* cut_tab;
+  unsigned char* axis_tab;
+  const double* xs_sorted;
+  const double* ys_sorted;
+  int L;
+};
+
+__device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long long j, int s0,
+                                                int n, int2 x_first, int2 x_last, int2 y_first,
+                                                int2 y_last, int2 x_kth, int2 y_kth,
+                                                DevStatus* st, int* cut_rank_out,
+                                                bool* along_y_out) {
+  const Rect r = a.rect_tab[step_base(s) + j];
+  const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
+  if ((s & 1) == 0 && (s >> 1) < a.L) {                             // tree.py:348
+    double xa = a.xs_sorted[x_first.x], xb = a.xs_sorted[x_last.x];
+    double ya = a.ys_sorted[y_first.y], yb = a.ys_sorted[y_last.y];
+    if (xa == xb && ya == yb) {
+      unsigned long long key = ((unsigned long long)(s >> 1) << 40) | (unsigned long long)j;
+      atomicMin(&st->degenerate_key, key);
+      atomicOr(&st->flags, ST_DEGENERATE);
+    }
+  }
+  const int cr = along_y ? y_kth.y : x_kth.x;
+  const double cut = along_y ? a.ys_sorted[cr] : a.xs_sorted[cr];  // tree.py:265
+  a.cut_tab[step_base(s) + j] = cut;
+  a.axis_tab[step_base(s) + j] = along_y;
+  Rect lo = r, hi = r;                                              // tree.py:281-285
+  if (along_y) { lo.y1 = cut; hi.y0 = cut; } else { lo.x1 = cut; hi.x0 = cut; }
+  a.rect_tab[step_base(s + 1) + 2 * j] = lo;
+  a.rect_tab[step_base(s + 1) + 2 * j + 1] = hi;
+  *cut_rank_out = cr;
+  *along_y_out = along_y;
+  (void)n; (void)s0;
+}
+
+__global__ void k_global_prepare(StepArgs a, int s, const int2* X0, const int2* X1,
+                                 const int2* Y0, const int2* Y1, const unsigned char* xpar,
+                                 const unsigned char* ypar, unsigned char* xpar_next,
+                                 unsigned char* ypar_next, int* cutrank, unsigned char* axis_cur,
+                                 DevStatus* st) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= (1ll << s)) return;
+  const int* off = a.off + off_base(s);
+  const int s0 = off[j], n = off[j + 1] - s0, k = (n + 1) / 2;
+  const unsigned char xp = xpar[j], yp = ypar[j];
+  const int2* X = xp ? X1 : X0;
+  const int2* Y = yp ? Y1 : Y0;
+  int cr;
+  bool along_y;
+  prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
+                  Y[s0 + k - 1], st, &cr, &along_y);
+  cutrank[j] = cr;
+  axis_cur[j] = along_y;
+  // the copy ordered along the split axis stays put; the other one moves
+  const unsigned char nxp = along_y ? (unsigned char)(1 - xp) : xp;
+  const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
+  xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
+  ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
+}
+
+// stable partition of the moving copy, tiles aligned to segments
+__device__ __forceinline__ bool part_flag(int2 e, bool along_y, int cr) {
+  return (along_y ? e.y : e.x) <= cr;
+}
+
+__global__ void __launch_bounds__(PART_THREADS)
+k_part_count(int s, const int* __restrict__ tile_seg, const int* __restrict__ tile_start,
+             const int* __restrict__ off_all, const int2* X0, const int2* X1, const int2* Y0,
+             const int2* Y1, const unsigned char* xpar, const unsigned char* ypar,
+             const int* __restrict__ cutrank, const unsigned char* __restrict__ axis_cur,
+             int* tile_cnt) {
+  const int t = blockIdx.x;
+  const int j = tile_seg[t];
+  const int* off = off_all + off_base(s);
+  const int end = off[j + 1];
+  const bool along_y = axis_cur[j];
+  const int2* M = along_y ? (xpar[j] ? X1 : X0) : (ypar[j] ? Y1 : Y0);
+  const int cr = cutrank[j];
+  const int base = tile_start[t] + threadIdx.x * PART_ITEMS;
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < PART_ITEMS; ++q) {
+    int i = base + q;
+    if (i < end && i < tile_start[t] + PART_TILE) c += part_flag(M[i], along_y, cr);
+  }
+  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  __shared__ int sw[PART_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int q = 0; q < PART_THREADS / 32; ++q) tot += sw[q];
+    tile_cnt[t] = tot;
+  }
+}
+
+// segmented exclusive scan of tile counts (tiles of one segment are contiguous)
+__global__ void k_part_scan(int ntiles, const int* __restrict__ tile_seg,
+                            const int* __restrict__ tile_cnt, int* tile_pre) {
+  __shared__ int s_carry_seg, s_carry;
+  __shared__ int s_val[1024], s_seg[1024];
+  if (threadIdx.x == 0) { s_carry_seg = -1; s_carry = 0; }
+  __syncthreads();
+  for (int b = 0; b < ntiles; b += blockDim.x) {
+    int t = b + threadIdx.x;
+    int v = t < ntiles ? tile_cnt[t] : 0;
+    int sg = t < ntiles ? tile_seg[t] : 0x7fffffff;
+    s_val[threadIdx.x] = v;
+    s_seg[threadIdx.x] = sg;
+    __syncthreads();
+    // inclusive segmented Hillis-Steele in smem
+    for (int d = 1; d < (int)blockDim.x; d <<= 1) {
+      int add = 0;
+      if ((int)threadIdx.x >= d && s_seg[threadIdx.x - d] == sg) add = s_val[threadIdx.x - d];
+      __syncthreads();
+      s_val[threadIdx.x] += add;
+      __syncthreads();
+    }
+    int incl = s_val[threadIdx.x];
+    int carry = (sg == s_carry_seg) ? s_carry : 0;
+    if (t < ntiles) tile_pre[t] = carry + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+      s_carry = carry + incl;
+      s_carry_seg = sg;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PART_THREADS)
+k_part_scatter(int s, const int* __restrict__ tile_seg, const int* __restrict__ tile_start,
+               const int* __restrict__ off_all, int2* X0, int2* X1, int2* Y0, int2* Y1,
+               const unsigned char* xpar, const unsigned char* ypar,
+               const int* __restrict__ cutrank, const unsigned char* __restrict__ axis_cur,
+               const int* __restrict__ tile_pre) {
+  const int t = blockIdx.x;
+  const int j = tile_seg[t];
+  const int* off = off_all + off_base(s);
+  const int s0 = off[j], end = off[j + 1], k = (end - s0 + 1) / 2;
+  const bool along_y = axis_cur[j];
+  const bool mp = along_y ? xpar[j] : ypar[j];
+  const int2* M = along_y ? (mp ? X1 : X0) : (mp ? Y1 : Y0);
+  int2* D = along_y ? (mp ? X0 : X1) : (mp ? Y0 : Y1);
+  const int cr = cutrank[j];
+  const int tstart = tile_start[t];
+  const int tend = min(end, tstart + PART_TILE);
+  const int base = tstart + threadIdx.x * PART_ITEMS;
+  int2 e[PART_ITEMS];
+  bool f[PART_ITEMS];
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < PART_ITEMS; ++q) {
+    int i = base + q;
+    f[q] = false;
+    if (i < tend) {
+      e[q] = M[i];
+      f[q] = part_flag(e[q], along_y, cr);
+      c += f[q];
+    }
+  }
+  // block exclusive scan of c
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = c;
+  for (int d = 1; d < 32; d <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  __shared__ int sw[PART_THREADS / 32];
+  if (lane == 31) sw[w] = incl;
+  __syncthreads();
+  int wpre = 0;
+  for (int q = 0; q < w; ++q) wpre += sw[q];
+  int lp = tile_pre[t] + wpre + incl - c;   // left elements of this segment before `base`
+#pragma unroll
+  for (int q = 0; q < PART_ITEMS; ++q) {
+    int i = base + q;
+    if (i < tend) {
+      int dst = f[q] ? s0 + lp : s0 + k + (i - s0) - lp;
+      D[dst] = e[q];
+      lp += f[q];
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// subtree kernel: all remaining split steps of one segment inside SMEM
+struct SubArgs {
+  StepArgs a;
+  int sb, S;
+  const int2 *X0, *X1, *Y0, *Y1;
+  const unsigned char *xpar, *ypar;
+  const int* perm_x;
+  const double2* pos;
+  const double* g;
+  double2* src_pos;
+  double* src_g;
+  int* src_perm;
+  int* leaf_of;           // fallback: leaf id per original index
+  bool in_smem_finalize;
+  int nmax;
+};
+
+__global__ void __launch_bounds__(SUB_THREADS)
+k_subtree(SubArgs A, DevStatus* st) {
+  extern __shared__ unsigned char smem_raw[];
+  const long long j0 = blockIdx.x;
+  const int* off_sb = A.a.off + off_base(A.sb);
+  const int g0 = off_sb[j0];
+  const int n = off_sb[j0 + 1] - g0;
+  const int nmax = A.nmax;
+  const int nseg_max = 1 << (A.S - A.sb);
+  int2* sx = reinterpret_cast<int2*>(smem_raw);
+  int2* sy = sx + nmax;
+  int2* scr = sy + nmax;
+  unsigned short* segid = reinterpret_cast<unsigned short*>(scr + nmax);
+  int* q_s0 = reinterpret_cast<int*>(segid + ((nmax + 1) & ~1));
+  int* q_k = q_s0 + nseg_max;
+  int* q_cr = q_k + nseg_max;
+  int* q_P = q_cr + nseg_max;
+  unsigned char* q_ax = reinterpret_cast<unsigned char*>(q_P + nseg_max);
+  __shared__ int s_warp[SUB_THREADS / 32];
+
+  {
+    const int2* X = A.xpar[j0] ? A.X1 : A.X0;
+    const int2* Y = A.ypar[j0] ? A.Y1 : A.Y0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      sx[i] = X[g0 + i];
+      sy[i] = Y[g0 + i];
+      segid[i] = 0;
+    }
+  }
+  __syncthreads();
+
+  const int chunk = (n + SUB_THREADS - 1) / SUB_THREADS;
+  const int c0 = min(n, (int)threadIdx.x * chunk), c1 = min(n, c0 + chunk);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  for (int s = A.sb; s < A.S; ++s) {
+    const int nloc = 1 << (s - A.sb);
+    const int* off = A.a.off + off_base(s);
+    for (int q = threadIdx.x; q < nloc; q += blockDim.x) {
+      const long long j = j0 * nloc + q;
+      const int s0 = off[j] - g0, nn = off[j + 1] - off[j], k = (nn + 1) / 2;
+      int cr;
+      bool along_y;
+      prepare_segment(A.a, s, j, s0, nn, sx[s0], sx[s0 + nn - 1], sy[s0], sy[s0 + nn - 1],
+                      sx[s0 + k - 1], sy[s0 + k - 1], st, &cr, &along_y);
+      q_s0[q] = s0;
+      q_k[q] = k;
+      q_cr[q] = cr;
+      q_ax[q] = along_y;
+    }
+    __syncthreads();
+    // pass 1: count flags of this thread's contiguous chunk
+    int c = 0;
+    for (int i = c0; i < c1; ++i) {
+      int q = segid[i];
+      bool ay = q_ax[q];
+      c += part_flag(ay ? sx[i] : sy[i], ay, q_cr[q]);
+    }
+    int incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      int o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    if (lane == 31) s_warp[w] = incl;
+    __syncthreads();
+    int pre = incl - c;
+    for (int q = 0; q < w; ++q) pre += s_warp[q];
+    // pass 2: prefix at every segment start
+    {
+      int P = pre;
+      for (int i = c0; i < c1; ++i) {
+        int q = segid[i];
+        if (q_s0[q] == i) q_P[q] = P;
+        bool ay = q_ax[q];
+        P += part_flag(ay ? sx[i] : sy[i], ay, q_cr[q]);
+      }
+    }
+    __syncthreads();
+    // pass 3: scatter the moving copy into scratch
+    {
+      int P = pre;
+      for (int i = c0; i < c1; ++i) {
+        int q = segid[i];
+        bool ay = q_ax[q];
+        int2 e = ay ? sx[i] : sy[i];
+        bool f = part_flag(e, ay, q_cr[q]);
+        int lp = P - q_P[q];
+        int s0 = q_s0[q];
+        int dst = f ? s0 + lp : s0 + q_k[q] + (i - s0) - lp;
+        scr[dst] = e;
+        P += f;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int q = segid[i];
+      if (q_ax[q]) sx[i] = scr[i]; else sy[i] = scr[i];
+      segid[i] = (unsigned short)(2 * q + (i - q_s0[q] >= q_k[q]));
+    }
+    __syncthreads();
+  }
+
+  // leaves: members sorted by original index (canonical order)
+  const int nleaf = 1 << (A.S - A.sb);
+  const int* offL = A.a.off + off_base(A.S);
+  int* sidx = reinterpret_cast<int*>(scr);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sidx[i] = A.perm_x[sx[i].x];
+  __syncthreads();
+  if (A.in_smem_finalize) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int q = segid[i];
+      const long long jl = j0 * nleaf + q;
+      const int l0 = offL[jl] - g0, l1 = offL[jl + 1] - g0;
+      const int me = sidx[i];
+      int rank = 0;
+      for (int t = l0; t < l1; ++t) rank += sidx[t] < me;
+      const int dst = g0 + l0 + rank;
+      A.src_perm[dst] = me;
+      A.src_pos[dst] = A.pos[me];
+      A.src_g[dst] = A.g[me];
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      A.leaf_of[sidx[i]] = (int)(j0 * nleaf + segid[i]);
+  }
+}
+
+// --------------------------------------------------------------------------
+// fallback finalize / evaluation points: leaf ids then stable sort by leaf
+__global__ void k_global_leaf_of(int S, const int* __restrict__ offS, const int2* X0,
+                                 const int2* X1, const unsigned char* __restrict__ xpar,
+                                 const int* __restrict__ perm_x, long long n, int* leaf_of) {
+  // used when every split ran globally: leaf = segment of the final step
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long lo = 0, hi = (1ll << S);
+  while (hi - lo > 1) {
+    long long mid = (lo + hi) >> 1;
+    if (offS[mid] <= i) lo = mid; else hi = mid;
+  }
+  const int2* X = xpar[lo] ? X1 : X0;
+  leaf_of[perm_x[X[i].x]] = (int)lo;
+}
+
+__global__ void k_iota_perm(int* v, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int)i;
+}
+
+__global__ void k_descend(const double2* __restrict__ pts, long long m, int S,
+                          const double* __restrict__ cut_tab,
+                          const unsigned char* __restrict__ axis_tab, unsigned int* keys,
+                          int* vals) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const double2 z = pts[e];
+  long long seg = 0;
+  for (int s = 0; s < S; ++s) {
+    const long long t = step_base(s) + seg;
+    const double c = axis_tab[t] ? z.y : z.x;
+    seg = 2 * seg + (c <= cut_tab[t] ? 0 : 1);     // tree.py:273 (coords <= cut)
+  }
+  keys[e] = (unsigned int)seg;
+  vals[e] = (int)e;
+}
+
+__global__ void k_iota_keys(const int* __restrict__ leaf_of, long long n, unsigned int* keys,
+                            int* vals) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (unsigned int)leaf_of[i];
+  vals[i] = (int)i;
+}
+
+__global__ void k_gather_points(const int* __restrict__ perm, long long m,
+                                const double2* __restrict__ pts, const double* __restrict__ g,
+                                double2* out_pos, double* out_g, int* out_perm) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int e = perm[i];
+  out_perm[i] = e;
+  out_pos[i] = pts[e];
+  if (g) out_g[i] = g[e];
+}
+
+// leaf offsets from leaf-sorted keys (handles empty leaves)
+__global__ void k_leaf_offsets(const unsigned int* __restrict__ skeys, long long m, long long nleaf,
+                               int* leaf_off) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > m) return;
+  long long prev = i == 0 ? -1 : (long long)skeys[i - 1];
+  long long cur = i == m ? nleaf : (long long)skeys[i];
+  for (long long b = prev + 1; b <= cur; ++b) leaf_off[b] = (int)i;
+}
+
+__global__ void k_leaf_offsets_identity(int* leaf_off, long long m) {
+  leaf_off[0] = 0;
+  leaf_off[1] = (int)m;
+}
+
+// per-level box geometry from the rectangles of even steps (tree.py:375-377)
+__global__ void k_level_geometry(int L, const Rect* __restrict__ rect_tab, double* cx, double* cy,
+                                 double* hw, double* hh, double* r) {
+  long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = level_base(L + 1);
+  if (gid >= total) return;
+  int l = 0;
+  while (level_base(l + 1) <= gid) ++l;
+  const long long k = gid - level_base(l);
+  const Rect rc = rect_tab[step_base(2 * l) + k];
+  cx[gid] = (rc.x0 + rc.x1) / 2;
+  cy[gid] = (rc.y0 + rc.y1) / 2;
+  const double w = (rc.x1 - rc.x0) / 2, h = (rc.y1 - rc.y0) / 2;
+  hw[gid] = w;
+  hh[gid] = h;
+  r[gid] = glibc_hypot(w, h);
+}
+
+inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <class K, class V>
+void radix_sort_pairs(DBuf& tmp, const K* kin, K* kout, const V* vin, V* vout, long long n,
+                      int end_bit, cudaStream_t st) {
+  size_t bytes = 0;
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0,
+                                           end_bit, st));
+  tmp.reserve(bytes);
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, kin, kout, vin, vout, (int)n, 0,
+                                           end_bit, st));
+}
+
+int smem_need(long long nmax, int nseg) {
+  return (int)(3 * 8 * nmax + 2 * ((nmax + 1) & ~1ll) + 17ll * nseg + 64);
+}
+
+}  // namespace
+
+int plan_levels(int64_t n, int nd) {
+  // Eq. (6), tree.py:149-157, clamped so that 4^L <= n (tree.py:249-255)
+  double raw = 0.5 * std::log2(0.625 * (double)n / (double)nd);
+  int lev = raw > 0 ? (int)std::ceil(raw) : 0;
+  while (lev > 0 && (int64_t(1) << (2 * lev)) > n) --lev;
+  return lev;
+}
+
+void plan_tree(TreePlan& P, int64_t n, int64_t m, int L) {
+  if (P.n == n && P.m == m && P.L == L) return;
+  P.n = n; P.m = m; P.L = L; P.S = 2 * L;
+  const int S = P.S;
+  // choose the first step whose segments fit one subtree CTA in SMEM
+  auto nmax_at = [&](int s) { return (n + (int64_t(1) << s) - 1) >> s; };
+  int sb = S;
+  bool fits_any = false;
+  for (int s = 0; s <= S; ++s) {
+    if (smem_need(nmax_at(s), 1 << (S - s)) <= SMEM_BUDGET) { sb = s; fits_any = true; break; }
+  }
+  if (!fits_any) {
+    for (int s = 0; s <= S; ++s)
+      if (smem_need(nmax_at(s), 1 << (S - s)) <= 220 * 1024) { sb = s; fits_any = true; break; }
+  }
+  const int64_t leaf_max = nmax_at(S);
+  P.global_leaf_finalize = !fits_any || leaf_max > LEAF_SMEM_MAX;
+  if (!fits_any) sb = S;
+  P.sb = sb;
+  P.smem_bytes = fits_any ? smem_need(nmax_at(sb), 1 << (S - sb)) : 0;
+
+  // data-independent offsets for all steps (host mirror for the tile tables)
+  std::vector<std::vector<int64_t>> off(S + 1);
+  off[0] = {0, n};
+  for (int s = 0; s < S; ++s) {
+    const auto& o = off[s];
+    std::vector<int64_t> nx(2 * (o.size() - 1) + 1);
+    nx[0] = 0;
+    for (size_t j = 0; j + 1 < o.size(); ++j) {
+      int64_t cnt = o[j + 1] - o[j], left = (cnt + 1) / 2;
+      nx[2 * j + 1] = o[j] + left;
+      nx[2 * j + 2] = o[j + 1];
+    }
+    off[s + 1] = std::move(nx);
+  }
+  std::vector<int> tseg, tstart;
+  P.tile_base.assign(sb, 0);
+  P.tile_count.assign(sb, 0);
+  for (int s = 0; s < sb; ++s) {
+    P.tile_base[s] = (int)tseg.size();
+    for (size_t j = 0; j + 1 < off[s].size(); ++j) {
+      for (int64_t b = off[s][j]; b < off[s][j + 1]; b += PART_TILE) {
+        tseg.push_back((int)j);
+        tstart.push_back((int)b);
+      }
+    }
+    P.tile_count[s] = (int)tseg.size() - P.tile_base[s];
+  }
+  const int64_t off_entries = off_base(S + 1);
+  P.d_off.reserve(sizeof(int) * off_entries);
+  {
+    std::vector<int> flat(off_entries);
+    for (int s = 0; s <= S; ++s)
+      for (size_t j = 0; j < off[s].size(); ++j) flat[off_base(s) + j] = (int)off[s][j];
+    FMM_CUDA(cudaMemcpy(P.d_off.p, flat.data(), sizeof(int) * off_entries,
+                        cudaMemcpyHostToDevice));
+  }
+  P.d_tile_seg.reserve(sizeof(int) * (tseg.size() + 1));
+  P.d_tile_start.reserve(sizeof(int) * (tstart.size() + 1));
+  if (!tseg.empty()) {
+    FMM_CUDA(cudaMemcpy(P.d_tile_seg.p, tseg.data(), sizeof(int) * tseg.size(),
+                        cudaMemcpyHostToDevice));
+    FMM_CUDA(cudaMemcpy(P.d_tile_start.p, tstart.data(), sizeof(int) * tstart.size(),
+                        cudaMemcpyHostToDevice));
+  }
+}
+
+void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
+  const long long n = T.n, m = T.m;
+  const int L = T.L, S = 2 * L, sb = P.sb;
+  const double2* pos = T.pos_p;
+  const double2* epos = T.aliased ? pos : T.epos_p;
+  const long long nseg_total = step_base(S + 1);
+
+  T.src_pos.reserve(sizeof(double2) * n);
+  T.src_g.reserve(sizeof(double) * n);
+  T.src_perm.reserve(sizeof(int) * n);
+  T.eval_pos.reserve(sizeof(double2) * m);
+  T.eval_perm.reserve(sizeof(int) * m);
+  T.eval_leaf_off.reserve(sizeof(int) * ((1ll << S) + 1));
+  T.rect_tab.reserve(sizeof(Rect) * nseg_total);
+  T.cut_tab.reserve(sizeof(double) * (step_base(S) + 1));
+  T.axis_tab.reserve(step_base(S) + 1);
+  const long long nbox = level_base(L + 1);
+  for (DBuf* b : {&T.box_cx, &T.box_cy, &T.box_hw, &T.box_hh, &T.box_r})
+    b->reserve(sizeof(double) * nbox);
+  T.bbox.reserve(sizeof(double) * (4 + 4 * 1024) + 64);
+  const long long nmx = std::max(n, m);
+  T.keys_in.reserve(sizeof(unsigned long long) * nmx);
+  T.keys_out.reserve(sizeof(unsigned long long) * nmx);
+  T.vals_in.reserve(sizeof(int) * nmx);
+  T.vals_out.reserve(sizeof(int) * nmx);
+
+  // root rectangle
+  {
+    double* bb = T.bbox.as<double>();
+    unsigned int* counter = reinterpret_cast<unsigned int*>(bb + 4 + 4 * 1024);
+    FMM_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
+    unsigned blocks = (unsigned)std::min<long long>(1024, std::max<long long>(1, nblk(n + m, 256)));
+    k_bbox<<<blocks, 256, 0, st>>>(pos, n, epos, T.aliased ? 0 : m, bb, counter, bb + 4);
+    k_root_rect<<<1, 1, 0, st>>>(bb, T.rect_tab.as<Rect>());
+  }
+
+  if (S > 0) {
+    // global ranks along x and y (ties by original index: stable radix sort)
+    T.xs_sorted.reserve(sizeof(double) * n);
+    T.ys_sorted.reserve(sizeof(double) * n);
+    for (DBuf* b : {&T.perm_x, &T.perm_y, &T.rank_x, &T.rank_y}) b->reserve(sizeof(int) * n);
+    for (int axis = 0; axis < 2; ++axis) {
+      auto* kin = T.keys_in.as<unsigned long long>();
+      auto* kout = T.keys_out.as<unsigned long long>();
+      k_make_keys<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, kin, T.vals_in.as<int>());
+      int* perm = axis ? T.perm_y.as<int>() : T.perm_x.as<int>();
+      radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 64, st);
+      k_rank_scatter<<<nblk(n, 256), 256, 0, st>>>(
+          pos, n, axis, perm, axis ? T.ys_sorted.as<double>() : T.xs_sorted.as<double>(),
+          axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
+    }
+    for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
+    const long long pmax = (1ll << std::max(sb, 1)) + 2;
+    for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
+    T.cutrank.reserve(sizeof(int) * pmax + pmax);
+    k_init_arrays<<<nblk(n, 256), 256, 0, st>>>(n, T.perm_x.as<int>(), T.perm_y.as<int>(),
+                                                T.rank_x.as<int>(), T.rank_y.as<int>(),
+                                                T.X0.as<int2>(), T.Y0.as<int2>(),
+                                                T.xpar0.as<unsigned char>(),
+                                                T.ypar0.as<unsigned char>());
+    StepArgs a{P.d_off.as<int>(), T.rect_tab.as<Rect>(), T.cut_tab.as<double>(),
+               T.axis_tab.as<unsigned char>(), T.xs_sorted.as<double>(), T.ys_sorted.as<double>(),
+               L};
+    unsigned char *xp = T.xpar0.as<unsigned char>(), *yp = T.ypar0.as<unsigned char>();
+    unsigned char *xq = T.xpar1.as<unsigned char>(), *yq = T.ypar1.as<unsigned char>();
+    int* cutrank = T.cutrank.as<int>();
+    unsigned char* axis_cur = reinterpret_cast<unsigned char*>(cutrank + pmax);
+    int maxtiles = 1;
+    for (int s = 0; s < sb; ++s) maxtiles = std::max(maxtiles, P.tile_count[s]);
+    T.tile_cnt.reserve(sizeof(int) * maxtiles);
+    T.tile_pre.reserve(sizeof(int) * maxtiles);
+    const int2 *X0 = T.X0.as<int2>(), *X1 = T.X1.as<int2>(), *Y0 = T.Y0.as<int2>(),
+               *Y1 = T.Y1.as<int2>();
+    for (int s = 0; s < sb; ++s) {
+      k_global_prepare<<<nblk(1ll << s, 128), 128, 0, st>>>(a, s, X0, X1, Y0, Y1, xp, yp, xq, yq,
+                                                           cutrank, axis_cur, dstat);
+      const int nt = P.tile_count[s];
+      const int* tseg = P.d_tile_seg.as<int>() + P.tile_base[s];
+      const int* tstart = P.d_tile_start.as<int>() + P.tile_base[s];
+      k_part_count<<<nt, PART_THREADS, 0, st>>>(s, tseg, tstart, P.d_off.as<int>(), X0, X1, Y0,
+                                                Y1, xp, yp, cutrank, axis_cur,
+                                                T.tile_cnt.as<int>());
+      k_part_scan<<<1, 1024, 0, st>>>(nt, tseg, T.tile_cnt.as<int>(), T.tile_pre.as<int>());
+      k_part_scatter<<<nt, PART_THREADS, 0, st>>>(
+          s, tseg, tstart, P.d_off.as<int>(), T.X0.as<int2>(), T.X1.as<int2>(), T.Y0.as<int2>(),
+          T.Y1.as<int2>(), xp, yp, cutrank, axis_cur, T.tile_pre.as<int>());
+      std::swap(xp, xq);
+      std::swap(yp, yq);
+    }
+    T.leaf_of.reserve(sizeof(int) * std::max(n, m));
+    if (P.smem_bytes > 0) {
+      SubArgs A{a, sb, S, X0, X1, Y0, Y1, xp, yp, T.perm_x.as<int>(), pos, T.g_p,
+                T.src_pos.as<double2>(), T.src_g.as<double>(), T.src_perm.as<int>(),
+                T.leaf_of.as<int>(), !P.global_leaf_finalize,
+                (int)((n + (1ll << sb) - 1) >> sb)};
+      FMM_CUDA(cudaFuncSetAttribute(k_subtree, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    P.smem_bytes));
+      k_subtree<<<(unsigned)(1ll << sb), SUB_THREADS, P.smem_bytes, st>>>(A, dstat);
+    } else {
+      // every split ran as a global step: leaves are segments of the global copies
+      k_global_leaf_of<<<nblk(n, 256), 256, 0, st>>>(S, P.d_off.as<int>() + off_base(S), X0, X1,
+                                                     xp, T.perm_x.as<int>(), n,
+                                                     T.leaf_of.as<int>());
+    }
+    if (P.global_leaf_finalize) {
+      auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
+      auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
+      k_iota_keys<<<nblk(n, 256), 256, 0, st>>>(T.leaf_of.as<int>(), n, kin, T.vals_in.as<int>());
+      radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), n, S, st);
+      k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_out.as<int>(), n, pos, T.g_p,
+                                                    T.src_pos.as<double2>(), T.src_g.as<double>(),
+                                                    T.src_perm.as<int>());
+    }
+    // evaluation points: descend the cut table, stable sort by leaf
+    {
+      auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
+      auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
+      k_descend<<<nblk(m, 256), 256, 0, st>>>(epos, m, S, T.cut_tab.as<double>(),
+                                              T.axis_tab.as<unsigned char>(), kin,
+                                              T.vals_in.as<int>());
+      radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), m, S, st);
+      k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_out.as<int>(), m, epos, nullptr,
+                                                    T.eval_pos.as<double2>(), nullptr,
+                                                    T.eval_perm.as<int>());
+      k_leaf_offsets<<<nblk(m + 1, 256), 256, 0, st>>>(kout, m, 1ll << S, T.eval_leaf_off.as<int>());
+    }
+  } else {
+    // L == 0: a single box, identity permutations (tree.py:316-317)
+    k_iota_perm<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n);
+    k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n, pos, T.g_p,
+                                                  T.src_pos.as<double2>(), T.src_g.as<double>(),
+                                                  T.src_perm.as<int>());
+    k_iota_perm<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m);
+    k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m, epos, nullptr,
+                                                  T.eval_pos.as<double2>(), nullptr,
+                                                  T.eval_perm.as<int>());
+    k_leaf_offsets_identity<<<1, 1, 0, st>>>(T.eval_leaf_off.as<int>(), m);
+  }
+  k_level_geometry<<<nblk(nbox, 256), 256, 0, st>>>(L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
+                                                    T.box_cy.as<double>(), T.box_hw.as<double>(),
+                                                    T.box_hh.as<double>(), T.box_r.as<double>());
+}
+
+}  // namespace fmm
