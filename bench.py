@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark: FMM particles/sec of the full adaptive FMM pipeline on B200.
+
+Contract (one JSON line on rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1|c2|c3|c4|c5] [--n N]
+For N > 1 launch with torch.distributed.run; each rank evaluates its own
+independent problem of the configured size (replicas).
+
+A "step" is one full fmm_evaluate (tree build through P2P and un-permute) of
+the configured point set.  `value` is measured with inputs resident in HBM
+(device pointers) and CUDA events on the engine's stream; `e2e` goes through
+the public drop-in API fmm_evaluate(ParticleSet(...)) with pinned host
+buffers, host<->device copies inside the timed region.  L2 (126 MB) is
+flushed between timed steps by writing a 512 MiB buffer.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "c1": dict(kind="uniform", n=10_000, m=None, p=17, desc="uniform N=1e4, p=17 (CPU-runnable case)"),
+    "c2": dict(kind="uniform", n=1_000_000, m=None, p=20, desc="uniform N=1e6, p=20, single B200"),
+    "c3": dict(kind="normal", n=1_000_000, m=None, p=20, desc="normal sigma^2=0.01 N=1e6, p=20"),
+    "c4": dict(kind="uniform", n=1_000_000, m=1_000_000, p=30,
+               desc="uniform N=M=1e6 separate evaluation points, p=30"),
+    "c5": dict(kind="uniform", n=10_000_000, m=None, p=20, desc="uniform N=1e7, p=20"),
+}
+METRIC = "FMM particles/sec (FP64, p≈20) at 1/2/4/8 B200; per-phase roofline fraction"
+FP64_PEAK_FILE = ROOT / "profiles" / "r01_fp64_peak.json"
+
+
+def m2l_flops_per_pair(p):          # 2p(p+1) + 18p
+    return 2 * p * (p + 1) + 18 * p
+
+
+def p2p_flops_per_interaction():
+    return 11
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_points(cfg, seed):
+    import paper_1205_4611_b200 as F
+    pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, seed), cfg["n"])
+    if cfg["m"] is None:
+        return pts
+    ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, seed + 1), cfg["m"]).positions
+    return F.ParticleSet(pts.positions, pts.strengths, ev)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def run_ours(args, cfg, ws, rank, local):
+    import torch
+    import paper_1205_4611_b200 as F
+    from paper_1205_4611_b200.engine import fmm_evaluate_device
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    tcfg = F.TreeConfig(35, 0.5, cfg["p"])
+    pts = make_points(cfg, seed=rank)
+    n, m = pts.n_sources, pts.n_evals
+    alias = pts.evals_alias_sources
+
+    # device-resident inputs (value) -------------------------------------------
+    d_pos = torch.from_numpy(pts.positions.view(np.float64).reshape(-1, 2)).to(dev)
+    d_g = torch.from_numpy(pts.strengths).to(dev)
+    d_ev = None if alias else torch.from_numpy(pts.eval_positions.view(np.float64).reshape(-1, 2)).to(dev)
+    d_out = torch.empty((m, 2), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+
+    def step_device(hist=False):
+        return fmm_evaluate_device(n, d_pos.data_ptr(), d_g.data_ptr(), m,
+                                   None if d_ev is None else d_ev.data_ptr(), d_out.data_ptr(),
+                                   tcfg, device=local, histograms=hist)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step_device()
+    clocks = ClockSampler(local)
+    reps = []
+    walls = []
+    barrier()
+    clocks.start()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = step_device()
+        walls.append(time.perf_counter() - t0)
+        reps.append(rep)
+    barrier()
+    clk = clocks.stop()
+    dev_ms = [r.device_seconds * 1e3 for r in reps]
+    ms_step = sum(dev_ms) / len(dev_ms)
+    phase_ms = {k: 1e3 * sum(r.phase_seconds[k] for r in reps) / len(reps)
+                for k in F.PHASE_NAMES[:-1]}
+
+    # end to end through the public API with pinned host buffers ----------------
+    h_pos = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
+    h_pos[:] = pts.positions
+    h_g = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    h_g[:] = pts.strengths
+    if alias:
+        ps = F.ParticleSet(h_pos, h_g)
+    else:
+        h_ev = torch.empty(m, dtype=torch.complex128, pin_memory=True).numpy()
+        h_ev[:] = pts.eval_positions
+        ps = F.ParticleSet(h_pos, h_g, h_ev)
+    h_out = torch.empty(m, dtype=torch.complex128, pin_memory=True).numpy()
+    for _ in range(max(1, args.warmup // 2)):
+        F.fmm_evaluate(ps, tcfg, device=local, out=h_out)
+    e2e_s = []
+    h2d = d2h = 0
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        vals, rep_e2e = F.fmm_evaluate(ps, tcfg, device=local, out=h_out)
+        e2e_s.append(time.perf_counter() - t0)
+        h2d, d2h = rep_e2e.h2d_bytes, rep_e2e.d2h_bytes
+    barrier()
+    e2e_mean = sum(e2e_s) / len(e2e_s)
+
+    # max over ranks
+    if ws > 1:
+        t = torch.tensor([ms_step, e2e_mean], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step, e2e_mean = float(t[0]), float(t[1])
+
+    last = reps[-1]
+    pairs = last.list_totals.get("weak", 0)
+    m2l_ms = phase_ms["m2l"]
+    achieved = pairs * m2l_flops_per_pair(cfg["p"]) / (m2l_ms * 1e-3) / 1e12
+    try:
+        peak = json.loads(FP64_PEAK_FILE.read_text())["dfma_tflops"]
+        peak_src = f"self-measured DFMA (= DMMA) FP64 peak, {FP64_PEAK_FILE.relative_to(ROOT)}"
+    except Exception:
+        peak, peak_src = 37.0, "nominal B200 FP64 (no measured FP64 peak found)"
+    out = {
+        "metric": METRIC,
+        "value": ws * n / (ms_step * 1e-3),
+        "unit": "particles/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference sample_points generator, Philox seed = rank)",
+        "config": {"workload": cfg["desc"], "name": args.config, "n_sources": n, "n_evals": m,
+                   "p": cfg["p"], "theta": 0.5, "n_desired": 35, "distribution": cfg["kind"],
+                   "levels": int(last.n_levels), "parallelism": f"replicas x{ws}",
+                   "l2": "flushed between timed steps (512 MiB write)"},
+        "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+        "e2e": {"value": ws * n / e2e_mean, "unit": "particles/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_mean * 1e3},
+        "roofline": {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic": f"{pairs} M2L pairs x {m2l_flops_per_pair(cfg['p'])} flop "
+                                    "(SURVEY 8(d)) per launch / M2L phase event time",
+                     "peak_source": peak_src},
+        "clocks": clk,
+        "gpu_launches": None,
+        "host_wall_ms_per_step": 1e3 * sum(walls) / len(walls),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_n)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return out if rank == 0 else None
+
+
+def cpu_baseline(cfg, n_sample):
+    """Oracle port of the reference CPU path on a bounded sample of the same
+    workload (same distribution and p, N = n_sample)."""
+    from oracle import fmm2d_oracle as O
+    import paper_1205_4611_b200 as F
+    n = min(n_sample, cfg["n"])
+    pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 0), n)
+    ev = None
+    if cfg["m"] is not None:
+        ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 1), min(n_sample, cfg["m"])).positions
+    t0 = time.perf_counter()
+    O.fmm(pts.positions, pts.strengths, ev, 35, 0.5, cfg["p"])
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/fmm2d_oracle.py full pipeline on {cfg['kind']} N={n} "
+                      f"(M={'N' if ev is None else len(ev)}), p={cfg['p']}, one call, {dt:.2f} s, "
+                      "numpy single-threaded"}
+
+
+def run_reference(args, cfg, ws, rank):
+    if rank != 0:
+        return None
+    from oracle import fmm2d_oracle as O
+    import paper_1205_4611_b200 as F
+    n = min(args.cpu_n, cfg["n"])
+    pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 0), n)
+    ev = None
+    if cfg["m"] is not None:
+        ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 1), n).positions
+    for _ in range(args.warmup):
+        O.fmm(pts.positions, pts.strengths, ev, 35, 0.5, cfg["p"])
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.fmm(pts.positions, pts.strengths, ev, 35, 0.5, cfg["p"])
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(ts) / len(ts)
+    val = n / (ms * 1e-3)
+    sample = (f"oracle port of the reference CPU path, {cfg['kind']} N={n} p={cfg['p']} "
+              f"(bounded sample of {args.config}), numpy single-threaded")
+    return {"metric": METRIC, "value": val, "unit": "particles/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["desc"], "name": args.config, "n_sources": n, "p": cfg["p"]},
+            "cpu_baseline": {"value": val, "unit": "particles/s", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "particles/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override N (and M)")
+    ap.add_argument("--cpu-n", type=int, default=100_000, help="CPU baseline sample size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+        if cfg["m"] is not None:
+            cfg["m"] = args.n
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, cfg, ws, rank)
+    else:
+        out = run_ours(args, cfg, ws, rank, local)
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -37,6 +37,12 @@ struct DevStatus {
   int pad1;
 };
 
+// list buffers overflowed earlier in this stream: every list consumer bails out
+// (the host regrows the buffers and reruns the whole evaluation)
+__device__ __forceinline__ bool lists_overflowed(const DevStatus* st) {
+  return (*(volatile const int*)&st->flags) & ST_OVERFLOW;
+}
+
 // ----------------------------------------------------------------------------
 // complex double in registers
 struct cplx {

@@ -37,7 +37,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
   const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long nb = 1ll << (2 * l);
-  if (b >= nb) return;
+  if (b >= nb || lists_overflowed(st)) return;
   const long long gb = level_base(l) + b;
   const long long lb = level_base(l);
   const double rt = geo.r[gb], xt = geo.cx[gb], yt = geo.cy[gb];
@@ -99,7 +99,7 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
   const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long nb = 1ll << (2 * L);
-  if (b >= nb) return;
+  if (b >= nb || lists_overflowed(st)) return;
   const long long lb = level_base(L);
   const double rt = geo.r[lb + b], xt = geo.cx[lb + b], yt = geo.cy[lb + b];
   const int a0 = s_off[b], a1 = s_off[b + 1];
@@ -161,7 +161,7 @@ __global__ void k_radius(const double* hw, const double* hh, double* r, long lon
 __global__ void k_histogram(const int* __restrict__ off, long long n, int kind, int* hist,
                             DevStatus* st) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || lists_overflowed(st)) return;
   const int len = off[i + 1] - off[i];
   atomicAdd(&hist[kind * HIST_BINS + min(len, HIST_BINS - 1)], 1);
   atomicMax(&st->max_len[kind], len);
@@ -182,13 +182,12 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   const int L = T.L;
   const long long nbox = level_base(L + 1);
   const long long nleaf = 1ll << (2 * L);
-  if (Ls.cap_weak == 0) {
-    Ls.cap_weak = std::max<long long>(1024, 64 * nbox);
-    Ls.cap_strong = std::max<long long>(1024, 48 * nleaf);
-    Ls.cap_p2p = std::max<long long>(1024, 32 * nleaf);
-    Ls.cap_p2l = std::max<long long>(1024, 8 * nleaf);
-    Ls.cap_m2p = Ls.cap_p2l;
-  }
+  // capacities: at least a generous estimate for this tree, else the high-water mark
+  Ls.cap_weak = std::max<long long>(Ls.cap_weak, std::max<long long>(4096, 64 * nbox));
+  Ls.cap_strong = std::max<long long>(Ls.cap_strong, std::max<long long>(4096, 48 * nleaf));
+  Ls.cap_p2p = std::max<long long>(Ls.cap_p2p, std::max<long long>(4096, 32 * nleaf));
+  Ls.cap_p2l = std::max<long long>(Ls.cap_p2l, std::max<long long>(4096, 8 * nleaf));
+  Ls.cap_m2p = std::max<long long>(Ls.cap_m2p, std::max<long long>(4096, 8 * nleaf));
   Ls.weak_off.reserve(sizeof(int) * (nbox + 1));
   Ls.weak_idx.reserve(sizeof(int) * Ls.cap_weak);
   Ls.weak_tgt.reserve(sizeof(int) * Ls.cap_weak);

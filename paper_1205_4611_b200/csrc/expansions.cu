@@ -68,7 +68,7 @@ k_p2l(int L, const int* __restrict__ offL, const int* __restrict__ l_off,
       const double* __restrict__ src_g, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* local, int p, DevStatus* st) {
   const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (b >= (1ll << (2 * L))) return;
+  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
   const long long lb = level_base(L);
   const double x0 = cx[lb + b], y0 = cy[lb + b];
   cplx loc[PM + 1];
@@ -224,6 +224,7 @@ k_m2l(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       const int* __restrict__ w_tgt, const double* __restrict__ cx,
       const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
       double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+  if (lists_overflowed(st)) return;
   const long long npairs = *total_ptr;
   const long long nitems = (npairs + 31) >> 5;
   const int lane = threadIdx.x & 31;
@@ -320,7 +321,9 @@ k_m2l(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
 
 __global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __restrict__ w_tgt,
                             const double2* __restrict__ partials,
-                            const unsigned char* __restrict__ item_flags, double2* local, int p) {
+                            const unsigned char* __restrict__ item_flags, double2* local, int p,
+                            const DevStatus* st) {
+  if (lists_overflowed(st)) return;
   const long long npairs = *total_ptr;
   const long long nitems = (npairs + 31) >> 5;
   for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < nitems;
@@ -355,7 +358,7 @@ k_l2p_m2p(int L, const int* __restrict__ eoff, const double2* __restrict__ eval_
           int p, DevStatus* st) {
   const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (b >= (1ll << (2 * L))) return;
+  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
   const int e0 = eoff[b], e1 = eoff[b + 1];
   if (e0 == e1) return;
   const long long lb = level_base(L);
@@ -437,7 +440,7 @@ struct Launch {
                                     E.p, dstat);
     k_m2l_fixup<<<std::max(1u, std::min(1024u, nblk(items, 128))), 128, 0, st>>>(
         total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
-        E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p);
+        E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, dstat);
   }
   static void l2l(const TreeState& T, ExpState& E, cudaStream_t st) {
     for (int l = 1; l < T.L; ++l)

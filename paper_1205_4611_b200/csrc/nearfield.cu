@@ -28,7 +28,7 @@ k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
       const double2* __restrict__ phi_in, double2* values, DevStatus* st) {
   const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (b >= (1ll << (2 * L))) return;
+  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
   const int e0 = eoff[b], e1 = eoff[b + 1];
   if (e0 == e1) return;
   const int q0 = n_off[b], q1 = n_off[b + 1];
