@@ -57,6 +57,8 @@ typedef struct fmm2d_report {
   int32_t max_len[4];             /* longest list of each kind */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  int64_t kernel_launches;        /* engine kernels launched by the last attempt
+                                     (excludes the CUB radix-sort kernels) */
 } fmm2d_report;
 
 /* context on CUDA device `device` (buffers, stream, events grow monotonically) */

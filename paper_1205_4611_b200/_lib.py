@@ -40,6 +40,7 @@ class Report(C.Structure):
         ("max_len", C.c_int32 * 4),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("kernel_launches", C.c_int64),
     ]
 
 

@@ -20,6 +20,7 @@ enum : int {
   ST_M2L_SINGULAR = 4,    // operators.py:329-330
   ST_M2P_SINGULAR = 8,    // operators.py:376-377
   ST_OVERFLOW = 16,       // a list buffer was too small: host regrows + reruns
+  ST_RANK_RETRY = 32,     // a run of equal 32-bit rank keys was too long: rerun exact
 };
 
 struct DevStatus {

@@ -157,14 +157,33 @@ __global__ void k_radius(const double* hw, const double* hh, double* r, long lon
   if (i < n) r[i] = glibc_hypot(hw[i], hh[i]);
 }
 
-// list-length histograms and maxima for EngineReport (engine.py:185-204)
-__global__ void k_histogram(const int* __restrict__ off, long long n, int kind, int* hist,
-                            DevStatus* st) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n || lists_overflowed(st)) return;
-  const int len = off[i + 1] - off[i];
-  atomicAdd(&hist[kind * HIST_BINS + min(len, HIST_BINS - 1)], 1);
-  atomicMax(&st->max_len[kind], len);
+// list-length histograms and maxima for EngineReport (engine.py:185-204):
+// warp-aggregated (match_any) into a block-private SMEM histogram, then one
+// global add per non-empty bin
+__global__ void __launch_bounds__(256)
+k_histogram(const int* __restrict__ off, long long n, int kind, int* hist, DevStatus* st) {
+  __shared__ int sh[HIST_BINS];
+  __shared__ int smax;
+  if (lists_overflowed(st)) return;
+  for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  int mx = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i - threadIdx.x < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const bool valid = i < n;
+    const int len = valid ? off[i + 1] - off[i] : -1;
+    const int bin = min(len, HIST_BINS - 1);
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
+    mx = max(mx, len);
+  }
+  for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  if ((threadIdx.x & 31) == 0) atomicMax(&smax, mx);
+  __syncthreads();
+  for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[kind * HIST_BINS + i], sh[i]);
+  if (threadIdx.x == 0) atomicMax(&st->max_len[kind], smax);
 }
 
 inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -173,6 +192,7 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void compute_radius(TreeState& T, cudaStream_t st) {
   const long long nbox = level_base(T.L + 1);
+  note_launch();
   k_radius<<<nblk(nbox, 256), 256, 0, st>>>(T.box_hw.as<double>(), T.box_hh.as<double>(),
                                             T.box_r.as<double>(), nbox);
 }
@@ -204,6 +224,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
 
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
   int* woff = Ls.weak_off.as<int>();
+  note_launch();
   k_root_lists<<<1, 1, 0, st>>>(woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
@@ -213,6 +234,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const int* ps_idx = Ls.s_idx[cur].as<int>();
     int* wcnt = Ls.cnt_a.as<int>();
     int* scnt = Ls.cnt_b.as<int>();
+    note_launch();
     k_classify<<<blocks, CONN_THREADS, 0, st>>>(l, geo, theta, ps_off, ps_idx, wcnt, scnt,
                                                 nullptr, nullptr, nullptr, 0, nullptr, nullptr,
                                                 0, dstat);
@@ -221,6 +243,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     scan_exclusive(wcnt, wo, nb, Ls.totals, st, wo);
     int* so = Ls.s_off[1 - cur].as<int>();
     scan_exclusive(scnt, so, nb, Ls.totals, st, nullptr);
+    note_launch();
     k_classify<<<blocks, CONN_THREADS, 0, st>>>(l, geo, theta, ps_off, ps_idx, nullptr, nullptr,
                                                 woff, Ls.weak_idx.as<int>(),
                                                 Ls.weak_tgt.as<int>(), Ls.cap_weak, so,
@@ -232,12 +255,14 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const unsigned blocks = nblk(nleaf * 32, CONN_THREADS);
     const int* s_off = Ls.s_off[cur].as<int>();
     const int* s_idx = Ls.s_idx[cur].as<int>();
+    note_launch();
     k_reclassify<<<blocks, CONN_THREADS, 0, st>>>(
         L, geo, theta, s_off, s_idx, Ls.cnt_a.as<int>(), Ls.cnt_b.as<int>(), Ls.cnt_c.as<int>(),
         nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, dstat);
     scan_exclusive(Ls.cnt_a.as<int>(), Ls.p2p_off.as<int>(), nleaf, Ls.totals, st);
     scan_exclusive(Ls.cnt_b.as<int>(), Ls.p2l_off.as<int>(), nleaf, Ls.totals, st);
     scan_exclusive(Ls.cnt_c.as<int>(), Ls.m2p_off.as<int>(), nleaf, Ls.totals, st);
+    note_launch();
     k_reclassify<<<blocks, CONN_THREADS, 0, st>>>(
         L, geo, theta, s_off, s_idx, nullptr, nullptr, nullptr, Ls.p2p_off.as<int>(),
         Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
@@ -249,13 +274,17 @@ void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t
   const long long nbox = level_base(T.L + 1);
   const long long nleaf = 1ll << (2 * T.L);
   FMM_CUDA(cudaMemsetAsync(Ls.hist.p, 0, sizeof(int) * 4 * HIST_BINS, st));
-  k_histogram<<<nblk(nbox, 256), 256, 0, st>>>(Ls.weak_off.as<int>(), nbox, 0, Ls.hist.as<int>(),
+  note_launch();
+  k_histogram<<<std::min(nblk(nbox, 256), 296u), 256, 0, st>>>(Ls.weak_off.as<int>(), nbox, 0, Ls.hist.as<int>(),
                                                dstat);
-  k_histogram<<<nblk(nleaf, 256), 256, 0, st>>>(Ls.p2p_off.as<int>(), nleaf, 1,
+  note_launch();
+  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.p2p_off.as<int>(), nleaf, 1,
                                                 Ls.hist.as<int>(), dstat);
-  k_histogram<<<nblk(nleaf, 256), 256, 0, st>>>(Ls.p2l_off.as<int>(), nleaf, 2,
+  note_launch();
+  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.p2l_off.as<int>(), nleaf, 2,
                                                 Ls.hist.as<int>(), dstat);
-  k_histogram<<<nblk(nleaf, 256), 256, 0, st>>>(Ls.m2p_off.as<int>(), nleaf, 3,
+  note_launch();
+  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.m2p_off.as<int>(), nleaf, 3,
                                                 Ls.hist.as<int>(), dstat);
 }
 

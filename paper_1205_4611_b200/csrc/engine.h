@@ -52,6 +52,7 @@ struct TreeState {
   int64_t n = 0, m = 0;
   int L = 0;
   bool aliased = true;
+  bool exact_keys = false;           // 64-bit rank keys (set after a tie-run overflow)
   DBuf pos, g, epos;                 // owned input copies, original order
   const double2* pos_p = nullptr;    // inputs actually used (owned copies or caller's
   const double* g_p = nullptr;       //   device memory), original order
@@ -67,6 +68,7 @@ struct TreeState {
   DBuf src_pos, src_g, src_perm;     // double2, double, int32
   DBuf eval_pos, eval_perm;          // double2, int32
   DBuf eval_leaf_off;                // int32[4^L + 1]
+  const unsigned* eval_leaf = nullptr;  // leaf of each tree-ordered eval point (L > 0)
   DBuf box_cx, box_cy, box_hw, box_hh, box_r;  // all levels, global box id
   DBuf bbox;                         // double[4] + scratch
 };
@@ -91,6 +93,10 @@ struct ExpState {
   DBuf values;                       // double2[M] input order
   DBuf partials, item_flags;         // M2L cross-warp partial sums
 };
+
+// count of engine kernel launches (gpu_launches evidence in the report)
+extern long long g_launches;
+inline void note_launch() { ++g_launches; }
 
 // ---------------------------------------------------------------------------
 // launchers (all enqueue on `st`, no host sync)

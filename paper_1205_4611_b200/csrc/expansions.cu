@@ -15,6 +15,9 @@
 // exact arithmetic.  B200 note (profiles/r01_fp64_peak.json): DMMA and DFMA
 // share one FP64 pipe (36.8 vs 36.5 TFLOP/s, 36.4 mixed), so the M2L stays a
 // register cascade on the vector pipe rather than an FP64 tensor-core GEMM.
+#include <cstdlib>
+#include <string>
+
 #include "engine.h"
 
 namespace fmm {
@@ -22,6 +25,31 @@ namespace fmm {
 namespace {
 
 constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:168-169
+// M2L variant: 0 = thread per pair, 1 = lane pair per pair over a flat pair
+// list, 2 = lane pair per pair, one warp per target (default);
+// FMM2D_M2L=pair|split|target overrides for A/B measurements
+int m2l_variant() {
+  static int v = [] {
+    const char* e = getenv("FMM2D_M2L");
+    if (e && std::string(e) == "pair") return 0;
+    if (e && std::string(e) == "split") return 1;
+    return 2;
+  }();
+  return v;
+}
+
+#ifndef M2L_MIN_BLOCKS
+#define M2L_MIN_BLOCKS 4
+#endif
+
+// branch-free lane-dependent selection: m all ones -> a, zero -> b
+__device__ __forceinline__ double dsel(double a, double b, unsigned long long m) {
+  const unsigned long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  return __longlong_as_double((x & m) | (y & ~m));
+}
+__device__ __forceinline__ double dxor(double a, unsigned long long s) {
+  return __longlong_as_double(__double_as_longlong(a) ^ s);
+}
 
 __device__ __forceinline__ cplx ld_coef(const double2* base, int j, int p) {
   if (j > p) return cplx{0.0, 0.0};
@@ -60,26 +88,31 @@ k_p2m(int L, const int* __restrict__ offL, const double2* __restrict__ src_pos,
     if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
 }
 
-// P2L (engine.py:85-93, operators.py:209-224): target-owned, sources ascending
+// P2L (engine.py:85-93, operators.py:209-224): one warp per target leaf, lanes
+// over the particles of its p2l source boxes (ascending), butterfly reduction
 template <int PM>
 __global__ void __launch_bounds__(128)
 k_p2l(int L, const int* __restrict__ offL, const int* __restrict__ l_off,
       const int* __restrict__ l_idx, const double2* __restrict__ src_pos,
       const double* __restrict__ src_g, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* local, int p, DevStatus* st) {
-  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
   const long long lb = level_base(L);
+  double2* out = local + (lb + b) * (p + 1);
+  const int q0 = l_off[b], q1 = l_off[b + 1];
+  if (q0 == q1) {                    // no p2l sources: local starts at zero
+    for (int j = lane; j <= p; j += 32) out[j] = make_double2(0.0, 0.0);
+    return;
+  }
   const double x0 = cx[lb + b], y0 = cy[lb + b];
-  cplx loc[PM + 1];
+  cplx acc[PM + 1];
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) loc[j] = cplx{0.0, 0.0};
-  for (int q = l_off[b]; q < l_off[b + 1]; ++q) {
+  for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
+  for (int q = q0; q < q1; ++q) {
     const int a = l_idx[q];
-    cplx box[PM + 1];
-#pragma unroll
-    for (int j = 0; j <= PM; ++j) box[j] = cplx{0.0, 0.0};
-    for (int i = offL[a]; i < offL[a + 1]; ++i) {
+    for (int i = offL[a] + lane; i < offL[a + 1]; i += 32) {
       const double2 z = src_pos[i];
       const cplx d{z.x - x0, z.y - y0};
       if (d.x == 0.0 && d.y == 0.0) {
@@ -90,17 +123,20 @@ k_p2l(int L, const int* __restrict__ offL, const int* __restrict__ l_off,
       cplx w = cscale(inv, src_g[i]);
 #pragma unroll
       for (int k = 0; k <= PM; ++k) {
-        box[k] = cadd(box[k], w);
+        acc[k] = cadd(acc[k], w);
         w = cmul(w, inv);
       }
     }
-#pragma unroll
-    for (int j = 0; j <= PM; ++j) loc[j] = cadd(loc[j], box[j]);
   }
-  double2* out = local + (lb + b) * (p + 1);
 #pragma unroll
-  for (int j = 0; j <= PM; ++j)
-    if (j <= p) out[j] = make_double2(loc[j].x, loc[j].y);
+  for (int j = 0; j <= PM; ++j) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, d);
+      acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, d);
+    }
+    if (j <= p && (j & 31) == lane) out[j] = make_double2(acc[j].x, acc[j].y);
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -219,7 +255,7 @@ k_l2l(int l, const double* __restrict__ cx, const double* __restrict__ cy, doubl
 // inside one warp are updated in place (exclusive ownership, no atomics);
 // targets spanning warps leave ordered partials that k_m2l_fixup folds in.
 template <int PM>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, M2L_MIN_BLOCKS)
 k_m2l(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       const int* __restrict__ w_tgt, const double* __restrict__ cx,
       const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
@@ -319,81 +355,295 @@ k_m2l(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   }
 }
 
+// Same M2L with a lane PAIR per interaction: the cascades are real-linear, so
+// lane 2i carries the real parts and lane 2i+1 the imaginary parts of pair i;
+// only the pre/post scalings mix them (one shuffle per coefficient).  Half
+// the registers of the thread-per-pair form, so twice the resident warps to
+// hide FP64 and L2 latency.  16 pairs per warp item.
+// Target-owned M2L (default).  One warp per target box walks the target's
+// weak list in chunks of 16 pairs; lane pair (2i, 2i+1) carries the real /
+// imaginary part of pair i (the cascades of operators.py:339-344 are
+// real-linear).  Each lane accumulates its pairs in order, then a fixed xor
+// butterfly over the 16 lane pairs folds them and the target row is updated
+// once -- no partials, no fixup, no atomics.
+template <int PM>
+__global__ void __launch_bounds__(128)
+k_m2l_target(long long nbox, const int* __restrict__ woff, const int* __restrict__ w_src,
+             const double* __restrict__ cx, const double* __restrict__ cy,
+             const double2* __restrict__ mult, double2* local, int p, DevStatus* st) {
+  if (lists_overflowed(st)) return;
+  const int lane = threadIdx.x & 31, h = lane & 1, pl = lane >> 1;
+  const unsigned long long hm = h ? ~0ull : 0ull;
+  const unsigned long long neg0 = h ? 0ull : 0x8000000000000000ull;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; t < nbox;
+       t += nwarps) {
+    const int q0 = woff[t], q1 = woff[t + 1];
+    if (q0 == q1) continue;
+    const double tx = cx[t], ty = cy[t];
+    double acc[PM + 1];
+#pragma unroll
+    for (int j = 0; j <= PM; ++j) acc[j] = 0.0;
+    bool sing_any = false;
+    for (int base = q0; base < q1; base += 16) {
+      const int q = base + pl;
+      const bool valid = q < q1;
+      const int s = valid ? w_src[q] : (int)t;
+      const cplx rho{cx[s] - tx, cy[s] - ty};                    // source - target
+      const bool sing = valid && rho.x == 0.0 && rho.y == 0.0;
+      sing_any |= sing;
+      const cplx inv = (valid && !sing) ? crcp(rho) : cplx{0.0, 0.0};
+      const double qx = -inv.x, qy = -inv.y;                     // q = -1/rho
+      const double2* a = mult + (long long)s * (p + 1);
+      double c[PM + 1];
+      {   // c_{k-1} = (a_k q^k)_h ; the lane pair shares the power sequence
+        double own = dsel(qy, qx, hm);
+#pragma unroll
+        for (int k = 1; k <= PM; ++k) {
+          const double part = __shfl_xor_sync(0xffffffffu, own, 1);
+          const double ps = dxor(part, neg0);
+          const cplx ak = ld_coef(a, k, p);
+          c[k - 1] = fma(ak.x, own, ak.y * ps);
+          own = fma(ps, qy, own * qx);
+        }
+        c[PM] = 0.0;
+      }
+#pragma unroll
+      for (int k = 2; k <= PM; ++k)               // pass 1, old values (operators.py:339-341)
+#pragma unroll
+        for (int j = PM - k; j < PM; ++j) c[j] += c[j + 1];
+#pragma unroll
+      for (int k = PM; k >= 1; --k)               // pass 2, new values (operators.py:342-344)
+#pragma unroll
+        for (int j = k; j <= PM; ++j) c[j] += c[j - 1];
+      {   // b_j = c_j / rho^j = c_j (-q)^j (operators.py:349-350)
+        acc[0] += c[0];
+        double own = dsel(qy, qx, hm);
+#pragma unroll
+        for (int j = 1; j <= PM; ++j) {
+          const double pp = __shfl_xor_sync(0xffffffffu, own, 1);
+          const double cp = __shfl_xor_sync(0xffffffffu, c[j], 1);
+          const double A = dsel(cp, c[j], hm);
+          const double B = dsel(c[j], dxor(cp, 0x8000000000000000ull), hm);
+          const double v = fma(A, own, B * pp);
+          acc[j] += (j & 1) ? -v : v;
+          own = fma(dxor(pp, neg0), qy, own * qx);
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, sing_any) && lane == 0) atomicOr(&st->flags, ST_M2L_SINGULAR);
+    // fold the 16 lane pairs (same component), fixed butterfly order
+#pragma unroll
+    for (int j = 0; j <= PM; ++j) {
+#pragma unroll
+      for (int d = 2; d < 32; d <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], d);
+    }
+    double* row = reinterpret_cast<double*>(local + t * (p + 1));
+#pragma unroll
+    for (int j = 0; j <= PM; ++j)
+      if (j <= p && (j & 15) == pl) row[2 * j + h] += acc[j];
+  }
+}
+
+// one coalesced row update of a target segment's sum (coefficient j, part comp)
+__device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
+                                         unsigned char* item_flags, long long item, int p, int t,
+                                         int j, int comp, double v, bool starts_before,
+                                         bool ends_after) {
+  if (!starts_before && !ends_after) {
+    double* dst = reinterpret_cast<double*>(local + (long long)t * (p + 1)) + 2 * j + comp;
+    *dst += v;
+    return;
+  }
+  const int slot = starts_before ? 0 : 1;
+  reinterpret_cast<double*>(partials + (item * 2 + slot) * (p + 1))[2 * j + comp] = v;
+  if (j == 0 && comp == 0) {
+    const unsigned f = starts_before ? (ends_after ? 5u : 1u) : 2u;
+    atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)), f << (8 * (item & 3)));
+  }
+}
+
+template <int PM>
+__global__ void __launch_bounds__(128)
+k_m2l_split(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
+            const int* __restrict__ w_tgt, const double* __restrict__ cx,
+            const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
+            double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+  if (lists_overflowed(st)) return;
+  extern __shared__ double red[];          // 4 warps x 32 lanes x RS doubles
+  __shared__ int s_tgt[4][16];
+  constexpr int RS = (PM + 1) | 1;         // odd row stride: conflict-free 8-byte banks
+  const long long npairs = *total_ptr;
+  const long long nitems = (npairs + 15) >> 4;
+  const int lane = threadIdx.x & 31, h = lane & 1, pl = lane >> 1;
+  const long long warps_total = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; item < nitems;
+       item += warps_total) {
+    const long long i = item * 16 + pl;
+    const bool valid = i < npairs;
+    // padding lanes run the same code on box 0 with a zero reciprocal
+    const int t = valid ? w_tgt[i] : -1;
+    const int s = valid ? w_src[i] : 0;
+    const int tt = valid ? t : 0;
+    const cplx rho{cx[s] - cx[tt], cy[s] - cy[tt]};               // source - target
+    const bool sing = valid && rho.x == 0.0 && rho.y == 0.0;
+    if (__any_sync(0xffffffffu, sing) && lane == 0) atomicOr(&st->flags, ST_M2L_SINGULAR);
+    const cplx inv = (valid && !sing) ? crcp(rho) : cplx{0.0, 0.0};
+    // q = -1/rho: q^k = (-1)^k / rho^k.  The lane pair shares the power
+    // sequence: each lane advances its own component, the partner's comes by
+    // shuffle, so a complex power costs 2 FP64 ops per lane instead of 4.
+    const double qx = -inv.x, qy = -inv.y;
+    const double2* a = mult + (long long)s * (p + 1);
+    double c[PM + 1];
+    // lane-dependent choices as bit masks (a select on h would make the
+    // compiler unswitch the unrolled loops and serialise both lane halves)
+    const unsigned long long hm = h ? ~0ull : 0ull;            // all ones on the imag lane
+    const unsigned long long neg0 = h ? 0ull : 0x8000000000000000ull;
+    {
+      double own = dsel(qy, qx, hm);                               // component h of q^1
+#pragma unroll
+      for (int k = 1; k <= PM; ++k) {
+        const double part = __shfl_xor_sync(0xffffffffu, own, 1);
+        const double ps = dxor(part, neg0);                        // partner, signed
+        const cplx ak = ld_coef(a, k, p);
+        c[k - 1] = fma(ak.x, own, ak.y * ps);                      // (a_k q^k)_h
+        own = fma(ps, qy, own * qx);                               // (q^{k+1})_h
+      }
+      c[PM] = 0.0;
+    }
+#pragma unroll
+    for (int k = 2; k <= PM; ++k)                 // pass 1, old values (operators.py:339-341)
+#pragma unroll
+      for (int j = PM - k; j < PM; ++j) c[j] += c[j + 1];
+#pragma unroll
+    for (int k = PM; k >= 1; --k)                 // pass 2, new values (operators.py:342-344)
+#pragma unroll
+      for (int j = k; j <= PM; ++j) c[j] += c[j - 1];
+    {   // postscale b_j = c_j / rho^j = c_j (-q)^j (operators.py:349-350)
+      double own = dsel(qy, qx, hm);
+#pragma unroll
+      for (int j = 1; j <= PM; ++j) {
+        const double pp = __shfl_xor_sync(0xffffffffu, own, 1);    // partner of q^j
+        const double cp = __shfl_xor_sync(0xffffffffu, c[j], 1);   // partner of c_j
+        // (c q^j)_h  h=0: c_o w_o - c_p w_p ;  h=1: c_p w_o + c_o w_p
+        const double A = dsel(cp, c[j], hm);
+        const double B = dsel(c[j], dxor(cp, 0x8000000000000000ull), hm);
+        const double v = fma(A, own, B * pp);
+        c[j] = (j & 1) ? -v : v;
+        own = fma(dxor(pp, neg0), qy, own * qx);
+      }
+    }
+    // per-target sums through SMEM: every lane parks its row, then lane r
+    // owns coefficient r>>1 (component r&1) and walks the 16 pairs in order,
+    // emitting one coalesced row update per target segment
+    double* row = red + ((threadIdx.x >> 5) * 32 + lane) * RS;
+#pragma unroll
+    for (int j = 0; j <= PM; ++j) row[j] = c[j];
+    int* wt = s_tgt[threadIdx.x >> 5];
+    if (h == 0) wt[pl] = t;
+    const int t0 = __shfl_sync(0xffffffffu, t, 0);
+    const bool first_cont = item > 0 && t0 >= 0 && w_tgt[item * 16 - 1] == t0;
+    const long long last = min(item * 16 + 15, npairs - 1);
+    const int t_last = w_tgt[last];
+    const bool last_cont = last + 1 < npairs && w_tgt[last + 1] == t_last;
+    __syncwarp();
+    const double* wred = red + (threadIdx.x >> 5) * 32 * RS;
+    for (int r = lane; r < 2 * (p + 1); r += 32) {
+      const int j = r >> 1, comp = r & 1;
+      double acc = 0.0;
+      int seg_t = wt[0], seg_first = 1;
+      for (int q = 0; q < 16; ++q) {
+        const int tq = wt[q];
+        if (tq < 0) break;
+        if (tq != seg_t) {     // segment ends before pair q
+          m2l_emit(local, partials, item_flags, item, p, seg_t, j, comp, acc,
+                   seg_first && first_cont, false);
+          seg_t = tq;
+          seg_first = 0;
+          acc = 0.0;
+        }
+        acc += wred[(2 * q + comp) * RS + j];
+      }
+      if (seg_t >= 0)
+        m2l_emit(local, partials, item_flags, item, p, seg_t, j, comp, acc,
+                 seg_first && first_cont, last_cont);
+    }
+    __syncwarp();
+  }
+}
+
+// ordered fold of the partial sums of targets whose pairs span several warp
+// items: one warp per item, lanes over coefficients (coalesced rows)
 __global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __restrict__ w_tgt,
                             const double2* __restrict__ partials,
                             const unsigned char* __restrict__ item_flags, double2* local, int p,
-                            const DevStatus* st) {
+                            int item_pairs, const DevStatus* st) {
   if (lists_overflowed(st)) return;
   const long long npairs = *total_ptr;
-  const long long nitems = (npairs + 31) >> 5;
-  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < nitems;
-       w += (long long)gridDim.x * blockDim.x) {
-    if (!(item_flags[w] & 2)) continue;          // chain head: tail segment continues
-    const int t = w_tgt[w * 32 + 31];
+  const long long nitems = (npairs + item_pairs - 1) / item_pairs;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nitems;
+       w += nwarps) {
+    if (!(item_flags[w] & 2)) continue;          // chain head: its tail segment continues
+    const int t = w_tgt[w * item_pairs + item_pairs - 1];
     double2* dst = local + (long long)t * (p + 1);
-    for (int j = 0; j <= p; ++j) {
-      double sx = partials[(w * 2 + 1) * (p + 1) + j].x;
-      double sy = partials[(w * 2 + 1) * (p + 1) + j].y;
+    for (int j = lane; j <= p; j += 32) {
+      double2 s = partials[(w * 2 + 1) * (p + 1) + j];
       for (long long u = w + 1; u < nitems; ++u) {
         const double2 v = partials[(u * 2 + 0) * (p + 1) + j];
-        sx += v.x;
-        sy += v.y;
+        s.x += v.x;
+        s.y += v.y;
         if (!(item_flags[u] & 4)) break;
       }
       const double2 o = dst[j];
-      dst[j] = make_double2(o.x + sx, o.y + sy);
+      dst[j] = make_double2(o.x + s.x, o.y + s.y);
     }
   }
 }
 
 // --------------------------------------------------------------------------
-// L2P + M2P (engine.py:132-160): warp per finest box, lanes over its points.
-// phi = L2P, then += each m2p source in ascending order (operators.py:358-386)
+// L2P + M2P (engine.py:132-160): one thread per evaluation point (tree order),
+// its leaf from the tree build.  phi = L2P (Horner in y - z0), then += each
+// m2p source in ascending order (operators.py:358-386).  Coefficients stream
+// from L1/L2 (the points of one leaf share them), so no register arrays.
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_l2p_m2p(int L, const int* __restrict__ eoff, const double2* __restrict__ eval_pos,
-          const int* __restrict__ m_off, const int* __restrict__ m_idx,
-          const double* __restrict__ cx, const double* __restrict__ cy,
-          const double2* __restrict__ mult, const double2* __restrict__ local, double2* phi,
-          int p, DevStatus* st) {
-  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
-  const int e0 = eoff[b], e1 = eoff[b + 1];
-  if (e0 == e1) return;
+k_l2p_m2p(long long m, int L, const unsigned* __restrict__ leaf,
+          const double2* __restrict__ eval_pos, const int* __restrict__ m_off,
+          const int* __restrict__ m_idx, const double* __restrict__ cx,
+          const double* __restrict__ cy, const double2* __restrict__ mult,
+          const double2* __restrict__ local, double2* phi, int p, DevStatus* st) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= m || lists_overflowed(st)) return;
   const long long lb = level_base(L);
-  const double x0 = cx[lb + b], y0 = cy[lb + b];
+  const long long b = leaf[e];
+  const double2 y = eval_pos[e];
+  const cplx w{y.x - cx[lb + b], y.y - cy[lb + b]};
   const double2* bl = local + (lb + b) * (p + 1);
-  cplx loc[PM + 1];
+  cplx c[PM + 1];
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) loc[j] = ld_coef(bl, j, p);
-  for (int e = e0 + lane; e < e1; e += 32) {
-    const double2 y = eval_pos[e];
-    cplx acc;
-    if (L > 0) {
-      const cplx w{y.x - x0, y.y - y0};
-      acc = loc[PM];
+  for (int j = 0; j <= PM; ++j) c[j] = ld_coef(bl, j, p);   // all loads in flight at once
+  cplx acc = c[PM];
 #pragma unroll
-      for (int j = PM - 1; j >= 0; --j) acc = cadd(cmul(acc, w), loc[j]);
-    } else {
-      acc = cplx{0.0, 0.0};
+  for (int j = PM - 1; j >= 0; --j) acc = cadd(cmul(acc, w), c[j]);
+  for (int q = m_off[b]; q < m_off[b + 1]; ++q) {
+    const long long ga = lb + m_idx[q];
+    const cplx u{y.x - cx[ga], y.y - cy[ga]};
+    if (u.x == 0.0 && u.y == 0.0) {
+      atomicOr(&st->flags, ST_M2P_SINGULAR);
+      continue;
     }
-    for (int q = m_off[b]; q < m_off[b + 1]; ++q) {
-      const long long ga = lb + m_idx[q];
-      const cplx u{y.x - cx[ga], y.y - cy[ga]};
-      if (u.x == 0.0 && u.y == 0.0) {
-        atomicOr(&st->flags, ST_M2P_SINGULAR);
-        continue;
-      }
-      const cplx inv = crcp(u);
-      const double2* a = mult + ga * (p + 1);
-      cplx h = ld_coef(a, PM, p);
+    const cplx inv = crcp(u);
+    const double2* a = mult + ga * (p + 1);
 #pragma unroll
-      for (int j = PM - 1; j >= 1; --j) h = cadd(cmul(h, inv), ld_coef(a, j, p));
-      acc = cadd(acc, cmul(h, inv));
-    }
-    phi[e] = make_double2(acc.x, acc.y);
+    for (int j = 1; j <= PM; ++j) c[j] = ld_coef(a, j, p);
+    cplx h = c[PM];
+#pragma unroll
+    for (int j = PM - 1; j >= 1; --j) h = cadd(cmul(h, inv), c[j]);
+    acc = cadd(acc, cmul(h, inv));
   }
+  phi[e] = make_double2(acc.x, acc.y);
 }
 
 inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -406,55 +656,82 @@ struct Launch {
     const int L = T.L, p = E.p;
     if (L == 0) return;
     const long long nleaf = 1ll << (2 * L);
+    note_launch();
     k_p2m<PM><<<nblk(nleaf, 128), 128, 0, st>>>(L, offL, T.src_pos.as<double2>(),
                                                 T.src_g.as<double>(), T.box_cx.as<double>(),
                                                 T.box_cy.as<double>(), E.mult.as<double2>(), p);
-    k_p2l<PM><<<nblk(nleaf, 128), 128, 0, st>>>(
+    note_launch();
+    k_p2l<PM><<<nblk(nleaf * 32, 128), 128, 0, st>>>(
         L, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.local.as<double2>(), p, dstat);
   }
   static void m2m(const TreeState& T, ExpState& E, cudaStream_t st) {
-    for (int l = T.L - 1; l >= 1; --l)
+    for (int l = T.L - 1; l >= 1; --l) {
+      note_launch();
       k_m2m<PM><<<nblk(1ll << (2 * l), 128), 128, 0, st>>>(l, T.box_cx.as<double>(),
                                                            T.box_cy.as<double>(),
                                                            E.mult.as<double2>(), E.p);
+    }
   }
   static void m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
                   cudaStream_t st) {
     const int L = T.L;
     if (L == 0) return;
     const int* total = Ls.weak_off.as<int>() + level_base(L + 1);
-    const long long items = (Ls.cap_weak + 31) / 32;
+    if (m2l_variant() == 2) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const long long nbox = level_base(L + 1);
+      const unsigned grid = (unsigned)std::min<long long>(nblk(nbox * 32, 128), 64ll * sms);
+      note_launch();
+      k_m2l_target<PM><<<grid, 128, 0, st>>>(nbox, Ls.weak_off.as<int>(), Ls.weak_idx.as<int>(),
+                                             T.box_cx.as<double>(), T.box_cy.as<double>(),
+                                             E.mult.as<double2>(), E.local.as<double2>(), E.p,
+                                             dstat);
+      return;
+    }
+    const bool split = m2l_variant() == 1;
+    const int item_pairs = split ? 16 : 32;
+    const long long items = (Ls.cap_weak + item_pairs - 1) / item_pairs;
     E.partials.reserve(sizeof(double2) * 2 * items * (E.p + 1));
     E.item_flags.reserve(((items + 4) & ~3ll) + 8);
     FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = (unsigned)std::min<long long>(nblk(items * 32, 128), 16ll * sms);
-    k_m2l<PM><<<grid, 128, 0, st>>>(total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(),
-                                    T.box_cx.as<double>(), T.box_cy.as<double>(),
-                                    E.mult.as<double2>(), E.local.as<double2>(),
-                                    E.partials.as<double2>(), E.item_flags.as<unsigned char>(),
-                                    E.p, dstat);
-    k_m2l_fixup<<<std::max(1u, std::min(1024u, nblk(items, 128))), 128, 0, st>>>(
+    const unsigned grid = (unsigned)std::min<long long>(nblk(items * 32, 128), 32ll * sms);
+    note_launch();
+    if (split) {
+      constexpr int RS = (PM + 1) | 1;
+      const int smem = 128 * RS * (int)sizeof(double);
+      if (smem > 48 * 1024)
+        FMM_CUDA(cudaFuncSetAttribute(k_m2l_split<PM>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_m2l_split<PM><<<grid, 128, smem, st>>>(total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(),
+                                            T.box_cx.as<double>(), T.box_cy.as<double>(),
+                                            E.mult.as<double2>(), E.local.as<double2>(),
+                                            E.partials.as<double2>(),
+                                            E.item_flags.as<unsigned char>(), E.p, dstat);
+    } else {
+      k_m2l<PM><<<grid, 128, 0, st>>>(total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(),
+                                      T.box_cx.as<double>(), T.box_cy.as<double>(),
+                                      E.mult.as<double2>(), E.local.as<double2>(),
+                                      E.partials.as<double2>(), E.item_flags.as<unsigned char>(),
+                                      E.p, dstat);
+    }
+    note_launch();
+    k_m2l_fixup<<<std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st>>>(
         total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
-        E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, dstat);
+        E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, item_pairs, dstat);
   }
   static void l2l(const TreeState& T, ExpState& E, cudaStream_t st) {
-    for (int l = 1; l < T.L; ++l)
+    for (int l = 1; l < T.L; ++l) {
+      note_launch();
       k_l2l<PM><<<nblk(1ll << (2 * (l + 1)), 128), 128, 0, st>>>(
           l, T.box_cx.as<double>(), T.box_cy.as<double>(), E.local.as<double2>(), E.p);
-  }
-  static void l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
-                      cudaStream_t st) {
-    const int L = T.L;
-    const long long nleaf = 1ll << (2 * L);
-    k_l2p_m2p<PM><<<nblk(nleaf * 32, 128), 128, 0, st>>>(
-        L, T.eval_leaf_off.as<int>(), T.eval_pos.as<double2>(), Ls.m2p_off.as<int>(),
-        Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
-        E.mult.as<double2>(), E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
+    }
   }
 };
 
@@ -495,7 +772,17 @@ void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st)
 }
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
                  cudaStream_t st) {
-  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::l2p_m2p(T, Ls, E, dstat, st); });
+  if (T.L == 0) {   // a single box: no expansions (engine.py:257)
+    FMM_CUDA(cudaMemsetAsync(E.phi.p, 0, sizeof(double2) * T.m, st));
+    return;
+  }
+  dispatch_p(E.p, [&](auto pm) {
+    note_launch();
+    k_l2p_m2p<decltype(pm)::value><<<nblk(T.m, 128), 128, 0, st>>>(
+        T.m, T.L, T.eval_leaf, T.eval_pos.as<double2>(), Ls.m2p_off.as<int>(),
+        Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
+        E.mult.as<double2>(), E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
+  });
 }
 
 }  // namespace fmm

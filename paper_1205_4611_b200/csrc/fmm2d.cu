@@ -20,6 +20,8 @@
 
 namespace fmm {
 
+long long g_launches = 0;
+
 CudaError::CudaError(cudaError_t e, const char* call, const char* file, int line) : err(e) {
   char buf[512];
   snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
@@ -220,6 +222,7 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
   DevStatus* dst = c->d_status.as<DevStatus>();
   int attempt = 0;
   for (;; ++attempt) {
+    g_launches = 0;
     reset_status(c);
     FMM_CUDA(cudaEventRecord(c->ev[0], c->st));
     build_tree_impl(c, nd);
@@ -249,6 +252,11 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     FMM_CUDA(cudaStreamSynchronize(c->st));
     FMM_CUDA(cudaGetLastError());
     const DevStatus& s = *c->h_status;
+    if (s.flags & ST_RANK_RETRY) {    // rare: clustered ties beyond the 32-bit keys
+      if (T.exact_keys) throw ApiError{FMM2D_ECUDA, "rank key retry did not converge"};
+      T.exact_keys = true;
+      continue;
+    }
     if ((s.flags & ST_DEGENERATE)) raise_degenerate(c);
     if (s.flags & ST_OVERFLOW) {
       if (attempt >= 8) throw ApiError{FMM2D_ECUDA, "interaction-list capacity did not converge"};
@@ -307,6 +315,7 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     r.list_totals[3] = tp[2];
   }
   for (int q = 0; q < 4; ++q) r.max_len[q] = s.max_len[q];
+  r.kernel_launches = g_launches;
   if (rep) *rep = r;
   return FMM2D_OK;
 }
@@ -387,11 +396,15 @@ int fmm2d_build_tree(fmm2d_ctx* c, int64_t n, const double* pos, const double* g
     FMM_CUDA(cudaSetDevice(c->device));
     int64_t h2d = 0;
     set_inputs(c, n, pos, g, m, epos, false, &h2d);
-    reset_status(c);
-    build_tree_impl(c, nd);
-    fetch_status(c);
-    FMM_CUDA(cudaStreamSynchronize(c->st));
-    FMM_CUDA(cudaGetLastError());
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      reset_status(c);
+      build_tree_impl(c, nd);
+      fetch_status(c);
+      FMM_CUDA(cudaStreamSynchronize(c->st));
+      FMM_CUDA(cudaGetLastError());
+      if (!(c->h_status->flags & ST_RANK_RETRY)) break;
+      c->T.exact_keys = true;
+    }
     c->have_tree = true;
     c->have_lists = c->have_eval = false;
     if (c->h_status->flags & ST_DEGENERATE) raise_degenerate(c);

@@ -18,20 +18,51 @@ namespace fmm {
 
 namespace {
 
-constexpr int P2P_THREADS = 128;
+constexpr int P2P_WARPS = 4;
+constexpr int P2P_THREADS = 32 * P2P_WARPS;
+constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// 1/r2 to ~1 ulp: MUFU reciprocal seed + two Newton steps on the FP64 pipe
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// One warp per target leaf.  The leaf's near sources (the concatenated source
+// ranges of its p2p boxes, ascending) are staged into a per-warp SMEM buffer
+// with cp.async, then every lane streams them from SMEM (broadcast reads).
 __global__ void __launch_bounds__(P2P_THREADS)
 k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
       const int* __restrict__ n_off, const int* __restrict__ n_idx,
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double2* __restrict__ eval_pos, const int* __restrict__ eval_perm,
       const double2* __restrict__ phi_in, double2* values, DevStatus* st) {
+  __shared__ double2 s_pos[P2P_WARPS][P2P_CHUNK];
+  __shared__ double s_g[P2P_WARPS][P2P_CHUNK];
   const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
   const int e0 = eoff[b], e1 = eoff[b + 1];
   if (e0 == e1) return;
   const int q0 = n_off[b], q1 = n_off[b + 1];
+  double2* sp = s_pos[w];
+  double* sg = s_g[w];
   unsigned long long skips = 0;
   for (int eb = e0; eb < e1; eb += 32) {
     const int ne = min(32, e1 - eb);
@@ -39,25 +70,55 @@ k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
     const bool active = lane < G * ne;
     const int ei = lane % ne, grp = lane / ne;
     double ax = 0.0, ay = 0.0;
-    double2 y = make_double2(0.0, 0.0);
-    if (active) {
-      y = eval_pos[eb + ei];
-      for (int q = q0; q < q1; ++q) {
+    const double2 y = eval_pos[eb + ei];
+    int q = q0, in_box = 0;
+    while (q < q1) {
+      // stage the next chunk of the concatenated near-source list
+      int fill = 0;
+      while (q < q1 && fill < P2P_CHUNK) {
         const int a = n_idx[q];
-        const int s1 = soff[a + 1];
-        for (int j = soff[a] + grp; j < s1; j += G) {
-          const double2 z = src_pos[j];
+        const int s0 = soff[a] + in_box, s1 = soff[a + 1];
+        const int take = min(s1 - s0, P2P_CHUNK - fill);
+        for (int t = lane; t < take; t += 32) {
+          cp_async16(sp + fill + t, src_pos + s0 + t);
+          cp_async8(sg + fill + t, src_g + s0 + t);
+        }
+        fill += take;
+        if (s0 + take == s1) { ++q; in_box = 0; } else { in_box += take; }
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      if (active) {
+        // four independent accumulator chains (fixed order, deterministic)
+        double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
+        int j = grp;
+        for (; j + 3 * G < fill; j += 4 * G) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2 z = sp[j + u * G];
+            const double dx = z.x - y.x, dy = z.y - y.y;
+            const double r2 = fma(dx, dx, dy * dy);
+            const bool coincide = r2 == 0.0;
+            skips += coincide;
+            const double gs = coincide ? 0.0 : sg[j + u * G] * rcp_nr(r2);
+            bx[u] = fma(gs, dx, bx[u]);
+            by[u] = fma(gs, dy, by[u]);
+          }
+        }
+        for (; j < fill; j += G) {
+          const double2 z = sp[j];
           const double dx = z.x - y.x, dy = z.y - y.y;
           const double r2 = fma(dx, dx, dy * dy);
-          if (r2 == 0.0) {
-            ++skips;
-            continue;
-          }
-          const double gs = src_g[j] / r2;
-          ax = fma(gs, dx, ax);
-          ay = fma(gs, dy, ay);
+          const bool coincide = r2 == 0.0;
+          skips += coincide;
+          const double gs = coincide ? 0.0 : sg[j] * rcp_nr(r2);
+          bx[0] = fma(gs, dx, bx[0]);
+          by[0] = fma(gs, dy, by[0]);
         }
+        ax += (bx[0] + bx[1]) + (bx[2] + bx[3]);
+        ay += (by[0] + by[1]) + (by[2] + by[3]);
       }
+      __syncwarp();
     }
     // fold the G lane groups of every point in fixed order
     for (int q = 1; q < G; ++q) {
@@ -116,6 +177,7 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st) {
   const long long nleaf = 1ll << (2 * T.L);
+  note_launch();
   k_p2p<<<nblk(nleaf * 32, P2P_THREADS), P2P_THREADS, 0, st>>>(
       T.L, offL, T.eval_leaf_off.as<int>(), Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(),
       T.src_pos.as<double2>(), T.src_g.as<double>(), T.eval_pos.as<double2>(),
@@ -124,6 +186,7 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
                 double2* out, cudaStream_t st) {
+  note_launch();
   k_direct<<<nblk(m, DIRECT_TILE), DIRECT_TILE, 0, st>>>(src, g, n, tgt, m, out);
 }
 

@@ -95,6 +95,7 @@ __global__ void write_base_total(int* out, const int* base_ptr) {
 void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t st,
                     const int* base) {
   if (n <= 0) {
+    note_launch();
     write_base_total<<<1, 1, 0, st>>>(out, base);
     return;
   }
@@ -104,6 +105,7 @@ void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t 
   FMM_CUDA(cudaMemsetAsync(tmp.p, 0, bytes, st));
   auto* status = tmp.as<unsigned long long>();
   auto* counter = reinterpret_cast<unsigned int*>(status + tiles);
+  note_launch();
   scan_tiles<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, status, counter, base);
 }
 

@@ -39,8 +39,35 @@ struct Rect {
 
 // --------------------------------------------------------------------------
 // bounding box of sources and evaluation points (tree.py:319-322)
-__global__ void k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__ epos,
-                       long long m, double* out, unsigned int* counter, double* partial) {
+__device__ __forceinline__ void block_minmax(double& x0, double& x1, double& y0, double& y1,
+                                             double (*sw)[32]) {
+  for (int d = 16; d; d >>= 1) {
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, d));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, d));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, d));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, d));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) { sw[0][w] = x0; sw[1][w] = x1; sw[2][w] = y0; sw[3][w] = y1; }
+  __syncthreads();
+  x0 = lane < nw ? sw[0][lane] : INFINITY;
+  x1 = lane < nw ? sw[1][lane] : -INFINITY;
+  y0 = lane < nw ? sw[2][lane] : INFINITY;
+  y1 = lane < nw ? sw[3][lane] : -INFINITY;
+  for (int d = 16; d; d >>= 1) {
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, d));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, d));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, d));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, d));
+  }
+}
+
+// tight bounding rectangle of sources and evaluation points (tree.py:319-322),
+// written straight into the root entry of the rectangle table
+__global__ void __launch_bounds__(256)
+k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__ epos,
+       long long m, Rect* root, unsigned int* counter, double* partial) {
   double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n + m;
        i += (long long)gridDim.x * blockDim.x) {
@@ -48,41 +75,28 @@ __global__ void k_bbox(const double2* __restrict__ pos, long long n, const doubl
     x0 = fmin(x0, z.x); x1 = fmax(x1, z.x);
     y0 = fmin(y0, z.y); y1 = fmax(y1, z.y);
   }
-  for (int d = 16; d; d >>= 1) {
-    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, d));
-    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, d));
-    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, d));
-    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, d));
-  }
   __shared__ double sw[4][32];
   __shared__ bool last;
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) { sw[0][w] = x0; sw[1][w] = x1; sw[2][w] = y0; sw[3][w] = y1; }
-  __syncthreads();
+  block_minmax(x0, x1, y0, y1, sw);
   if (threadIdx.x == 0) {
-    for (int q = 1; q < (int)blockDim.x / 32; ++q) {
-      x0 = fmin(x0, sw[0][q]); x1 = fmax(x1, sw[1][q]);
-      y0 = fmin(y0, sw[2][q]); y1 = fmax(y1, sw[3][q]);
-    }
     partial[4 * blockIdx.x + 0] = x0; partial[4 * blockIdx.x + 1] = x1;
     partial[4 * blockIdx.x + 2] = y0; partial[4 * blockIdx.x + 3] = y1;
     __threadfence();
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    for (unsigned q = 0; q < gridDim.x; ++q) {
-      x0 = fmin(x0, partial[4 * q + 0]); x1 = fmax(x1, partial[4 * q + 1]);
-      y0 = fmin(y0, partial[4 * q + 2]); y1 = fmax(y1, partial[4 * q + 3]);
-    }
-    out[0] = x0; out[1] = x1; out[2] = y0; out[3] = y1;
+  if (!last) return;
+  __threadfence();
+  x0 = INFINITY; x1 = -INFINITY; y0 = INFINITY; y1 = -INFINITY;
+  for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+    x0 = fmin(x0, __ldcg(partial + 4 * q + 0)); x1 = fmax(x1, __ldcg(partial + 4 * q + 1));
+    y0 = fmin(y0, __ldcg(partial + 4 * q + 2)); y1 = fmax(y1, __ldcg(partial + 4 * q + 3));
+  }
+  block_minmax(x0, x1, y0, y1, sw);
+  if (threadIdx.x == 0) {
+    *root = Rect{x0, x1, y0, y1};
     *counter = 0;
   }
-}
-
-__global__ void k_root_rect(const double* bbox, Rect* rect_tab) {
-  rect_tab[0] = Rect{bbox[0], bbox[1], bbox[2], bbox[3]};
 }
 
 // --------------------------------------------------------------------------
@@ -94,6 +108,69 @@ __global__ void k_make_keys(const double2* __restrict__ pos, long long n, int ax
   double2 z = pos[i];
   keys[i] = ordered_key(axis ? z.y : z.x);
   vals[i] = (int)i;
+}
+
+// 32-bit monotone key: fixed point of (c - lo) / (hi - lo) over the root
+// rectangle.  Non-decreasing in c (every step rounds monotonically), so a
+// stable sort by it orders the points up to runs of equal keys, which
+// k_fix_ties then orders exactly by (coordinate, index).
+__global__ void k_make_keys32(const double2* __restrict__ pos, long long n, int axis,
+                              const Rect* __restrict__ root, unsigned* keys, int* vals) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Rect r = *root;
+  const double lo = axis ? r.y0 : r.x0, span = axis ? r.y1 - r.y0 : r.x1 - r.x0;
+  const double2 z = pos[i];
+  const double c = axis ? z.y : z.x;
+  unsigned k = 0;
+  if (span > 0.0) {
+    const double u = (c - lo) / span * 4294967296.0;
+    k = u >= 4294967295.0 ? 0xffffffffu : (unsigned)u;
+  }
+  keys[i] = k;
+  vals[i] = (int)i;
+}
+
+constexpr int TIE_RUN_MAX = 64;
+
+// order every run of equal 32-bit keys by (coordinate, original index); a run
+// longer than TIE_RUN_MAX (pathologically clustered input) raises
+// ST_RANK_RETRY and the host reruns with exact 64-bit keys
+__global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
+                           const double2* __restrict__ pos, int axis, long long n,
+                           DevStatus* st) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned k = keys[i];
+  if ((i > 0 && keys[i - 1] == k) || i + 1 >= n || keys[i + 1] != k) return;
+  long long e = i + 1;
+  while (e < n && keys[e] == k) {
+    if (++e - i > TIE_RUN_MAX) {
+      atomicOr(&st->flags, ST_RANK_RETRY);
+      return;
+    }
+  }
+  const int cnt = (int)(e - i);
+  int idx[TIE_RUN_MAX];
+  double crd[TIE_RUN_MAX];
+  for (int q = 0; q < cnt; ++q) {
+    idx[q] = perm[i + q];
+    const double2 z = pos[idx[q]];
+    crd[q] = axis ? z.y : z.x;
+  }
+  for (int q = 1; q < cnt; ++q) {      // insertion sort, stable in index
+    const int vi = idx[q];
+    const double vc = crd[q];
+    int r = q - 1;
+    while (r >= 0 && (crd[r] > vc || (crd[r] == vc && idx[r] > vi))) {
+      idx[r + 1] = idx[r];
+      crd[r + 1] = crd[r];
+      --r;
+    }
+    idx[r + 1] = vi;
+    crd[r + 1] = vc;
+  }
+  for (int q = 0; q < cnt; ++q) perm[i + q] = idx[q];
 }
 
 __global__ void k_rank_scatter(const double2* __restrict__ pos, long long n, int axis,
@@ -670,8 +747,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     unsigned int* counter = reinterpret_cast<unsigned int*>(bb + 4 + 4 * 1024);
     FMM_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
     unsigned blocks = (unsigned)std::min<long long>(1024, std::max<long long>(1, nblk(n + m, 256)));
-    k_bbox<<<blocks, 256, 0, st>>>(pos, n, epos, T.aliased ? 0 : m, bb, counter, bb + 4);
-    k_root_rect<<<1, 1, 0, st>>>(bb, T.rect_tab.as<Rect>());
+    note_launch();
+    k_bbox<<<blocks, 256, 0, st>>>(pos, n, epos, T.aliased ? 0 : m, T.rect_tab.as<Rect>(),
+                                   counter, bb + 4);
   }
 
   if (S > 0) {
@@ -680,11 +758,24 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     T.ys_sorted.reserve(sizeof(double) * n);
     for (DBuf* b : {&T.perm_x, &T.perm_y, &T.rank_x, &T.rank_y}) b->reserve(sizeof(int) * n);
     for (int axis = 0; axis < 2; ++axis) {
-      auto* kin = T.keys_in.as<unsigned long long>();
-      auto* kout = T.keys_out.as<unsigned long long>();
-      k_make_keys<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, kin, T.vals_in.as<int>());
       int* perm = axis ? T.perm_y.as<int>() : T.perm_x.as<int>();
-      radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 64, st);
+      if (T.exact_keys) {
+        auto* kin = T.keys_in.as<unsigned long long>();
+        auto* kout = T.keys_out.as<unsigned long long>();
+        note_launch();
+        k_make_keys<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, kin, T.vals_in.as<int>());
+        radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 64, st);
+      } else {
+        auto* kin = reinterpret_cast<unsigned*>(T.keys_in.p);
+        auto* kout = reinterpret_cast<unsigned*>(T.keys_out.p);
+        note_launch();
+        k_make_keys32<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, T.rect_tab.as<Rect>(), kin,
+                                                    T.vals_in.as<int>());
+        radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 32, st);
+        note_launch();
+        k_fix_ties<<<nblk(n, 256), 256, 0, st>>>(kout, perm, pos, axis, n, dstat);
+      }
+      note_launch();
       k_rank_scatter<<<nblk(n, 256), 256, 0, st>>>(
           pos, n, axis, perm, axis ? T.ys_sorted.as<double>() : T.xs_sorted.as<double>(),
           axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
@@ -693,6 +784,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     const long long pmax = (1ll << std::max(sb, 1)) + 2;
     for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
     T.cutrank.reserve(sizeof(int) * pmax + pmax);
+    note_launch();
     k_init_arrays<<<nblk(n, 256), 256, 0, st>>>(n, T.perm_x.as<int>(), T.perm_y.as<int>(),
                                                 T.rank_x.as<int>(), T.rank_y.as<int>(),
                                                 T.X0.as<int2>(), T.Y0.as<int2>(),
@@ -712,15 +804,19 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     const int2 *X0 = T.X0.as<int2>(), *X1 = T.X1.as<int2>(), *Y0 = T.Y0.as<int2>(),
                *Y1 = T.Y1.as<int2>();
     for (int s = 0; s < sb; ++s) {
+      note_launch();
       k_global_prepare<<<nblk(1ll << s, 128), 128, 0, st>>>(a, s, X0, X1, Y0, Y1, xp, yp, xq, yq,
                                                            cutrank, axis_cur, dstat);
       const int nt = P.tile_count[s];
       const int* tseg = P.d_tile_seg.as<int>() + P.tile_base[s];
       const int* tstart = P.d_tile_start.as<int>() + P.tile_base[s];
+      note_launch();
       k_part_count<<<nt, PART_THREADS, 0, st>>>(s, tseg, tstart, P.d_off.as<int>(), X0, X1, Y0,
                                                 Y1, xp, yp, cutrank, axis_cur,
                                                 T.tile_cnt.as<int>());
+      note_launch();
       k_part_scan<<<1, 1024, 0, st>>>(nt, tseg, T.tile_cnt.as<int>(), T.tile_pre.as<int>());
+      note_launch();
       k_part_scatter<<<nt, PART_THREADS, 0, st>>>(
           s, tseg, tstart, P.d_off.as<int>(), T.X0.as<int2>(), T.X1.as<int2>(), T.Y0.as<int2>(),
           T.Y1.as<int2>(), xp, yp, cutrank, axis_cur, T.tile_pre.as<int>());
@@ -735,9 +831,11 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                 (int)((n + (1ll << sb) - 1) >> sb)};
       FMM_CUDA(cudaFuncSetAttribute(k_subtree, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     P.smem_bytes));
+      note_launch();
       k_subtree<<<(unsigned)(1ll << sb), SUB_THREADS, P.smem_bytes, st>>>(A, dstat);
     } else {
       // every split ran as a global step: leaves are segments of the global copies
+      note_launch();
       k_global_leaf_of<<<nblk(n, 256), 256, 0, st>>>(S, P.d_off.as<int>() + off_base(S), X0, X1,
                                                      xp, T.perm_x.as<int>(), n,
                                                      T.leaf_of.as<int>());
@@ -745,8 +843,10 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     if (P.global_leaf_finalize) {
       auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
       auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
+      note_launch();
       k_iota_keys<<<nblk(n, 256), 256, 0, st>>>(T.leaf_of.as<int>(), n, kin, T.vals_in.as<int>());
       radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), n, S, st);
+      note_launch();
       k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_out.as<int>(), n, pos, T.g_p,
                                                     T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                     T.src_perm.as<int>());
@@ -755,27 +855,38 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     {
       auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
       auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
+      note_launch();
       k_descend<<<nblk(m, 256), 256, 0, st>>>(epos, m, S, T.cut_tab.as<double>(),
                                               T.axis_tab.as<unsigned char>(), kin,
                                               T.vals_in.as<int>());
       radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), m, S, st);
+      note_launch();
       k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_out.as<int>(), m, epos, nullptr,
                                                     T.eval_pos.as<double2>(), nullptr,
                                                     T.eval_perm.as<int>());
+      note_launch();
       k_leaf_offsets<<<nblk(m + 1, 256), 256, 0, st>>>(kout, m, 1ll << S, T.eval_leaf_off.as<int>());
+      T.eval_leaf = kout;   // leaf id of every tree-ordered evaluation point
     }
   } else {
     // L == 0: a single box, identity permutations (tree.py:316-317)
+    note_launch();
     k_iota_perm<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n);
+    note_launch();
     k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n, pos, T.g_p,
                                                   T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                   T.src_perm.as<int>());
+    note_launch();
     k_iota_perm<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m);
+    note_launch();
     k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m, epos, nullptr,
                                                   T.eval_pos.as<double2>(), nullptr,
                                                   T.eval_perm.as<int>());
+    note_launch();
     k_leaf_offsets_identity<<<1, 1, 0, st>>>(T.eval_leaf_off.as<int>(), m);
+    T.eval_leaf = nullptr;
   }
+  note_launch();
   k_level_geometry<<<nblk(nbox, 256), 256, 0, st>>>(L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), T.box_hw.as<double>(),
                                                     T.box_hh.as<double>(), T.box_r.as<double>());

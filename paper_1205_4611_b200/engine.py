@@ -44,6 +44,7 @@ class EngineReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     retries: int = 0
+    kernel_launches: int = 0
 
 
 def _histograms(ctx: _lib.Context, rep: _lib.Report) -> dict[str, dict[int, int]]:
@@ -78,6 +79,7 @@ def _report(ctx, rep: _lib.Report, wall: float, points_alias: bool, m: int, para
         h2d_bytes=int(rep.h2d_bytes),
         d2h_bytes=int(rep.d2h_bytes),
         retries=int(rep.retries),
+        kernel_launches=int(rep.kernel_launches),
     )
 
 

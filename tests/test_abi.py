@@ -50,5 +50,5 @@ def test_binding_loads_and_host_only_calls_work():
 
 def test_report_struct_layout():
     # phase_ms, device_ms, total_ms, n_levels+retries, n_boxes, min, max, mean,
-    # skips, list_totals, max_len, h2d, d2h
-    assert ctypes.sizeof(_lib.Report) == 72 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 32 + 16 + 8 + 8
+    # skips, list_totals, max_len, h2d, d2h, kernel_launches
+    assert ctypes.sizeof(_lib.Report) == 72 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 32 + 16 + 8 + 8 + 8

@@ -140,3 +140,20 @@ def test_phase_expansions_match_oracle():
             assert np.max(np.abs(got - want) / scale) <= 1e-12, lev
     phi = F.engine.export_phi(pts.n_evals)
     assert np.all(np.isfinite(phi))
+
+
+def test_tie_runs_of_rank_keys_fall_back_to_exact_keys():
+    """300 points packed within 3e-11 in x (one run of equal 32-bit rank keys,
+    longer than the in-kernel fix-up handles) plus spread points: the engine
+    must rerun with exact 64-bit keys and still match the oracle."""
+    rng = np.random.default_rng(77)
+    x = np.concatenate([0.5 + 1e-13 * np.arange(300), rng.uniform(size=3000)])
+    y = rng.uniform(size=x.size)
+    pts = F.ParticleSet(x + 1j * y, rng.uniform(-1, 1, x.size))
+    cfg = F.TreeConfig(20, 0.5, 17)
+    T = O.build_tree(pts.positions, pts.strengths, None, 20)
+    tree = F.build_tree(pts, cfg)
+    assert_tree_equal(flat_tree_pkg(tree), flat_tree_oracle(T))
+    values, _ = F.fmm_evaluate(pts, cfg)
+    R = O.evaluate(T, O.build_connectivity(T, 0.5), 17)
+    assert max_rel(values, R.values) <= PARITY
