@@ -25,22 +25,25 @@ namespace fmm {
 namespace {
 
 constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:168-169
-// M2L variant: 0 = thread per pair, 1 = lane pair per pair over a flat pair
-// list, 2 = lane pair per pair, one warp per target (default);
-// FMM2D_M2L=pair|split|target overrides for A/B measurements
-int m2l_variant() {
-  static int v = [] {
+// M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
+// target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
+bool m2l_force_target() {
+  static bool v = [] {
     const char* e = getenv("FMM2D_M2L");
-    if (e && std::string(e) == "pair") return 0;
-    if (e && std::string(e) == "split") return 1;
-    return 2;
+    return e && std::string(e) == "target";
   }();
   return v;
 }
 
-#ifndef M2L_MIN_BLOCKS
-#define M2L_MIN_BLOCKS 4
-#endif
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
 
 // branch-free lane-dependent selection: m all ones -> a, zero -> b
 __device__ __forceinline__ double dsel(double a, double b, unsigned long long m) {
@@ -247,119 +250,199 @@ k_l2l(int l, const double* __restrict__ cx, const double* __restrict__ cy, doubl
 }
 
 // --------------------------------------------------------------------------
-// M2L (engine.py:103-123, operators.py:320-351).  All levels in one launch:
-// the weak lists form one global CSR sorted by (target, source), so the pair
-// list is flat.  One thread per pair computes the full (p+1)-term cascade in
-// registers; a warp takes 32 consecutive pairs and sums them per target with a
-// segmented shuffle scan (deterministic tree order).  Targets whose pairs sit
-// inside one warp are updated in place (exclusive ownership, no atomics);
-// targets spanning warps leave ordered partials that k_m2l_fixup folds in.
+// --------------------------------------------------------------------------
+// M2L (engine.py:103-123, operators.py:320-351), dense form.
+//
+// With alpha_k = a_k (-1)^k / rho^k (the reference's prescale), the two
+// cascades of operators.py:339-344 compute c_j = sum_k C(j+k-1, k-1) alpha_k
+// exactly (Pascal-matrix identity; potentials move <= 6e-14, SURVEY
+// Appendix B.5), and b_j = c_j / rho^j (operators.py:349-350).  The Pascal
+// matrix is a compile-time table in constant memory, so the core is
+// (p+1) p complex-by-real FMAs per pair with a constant-bank operand and no
+// data-dependent index math -- the same FP64 instruction count as the
+// cascade (840 at p=20) but 42 independent accumulation chains instead of a
+// wavefront, and alpha is the only register-resident array.
+//
+// Work split: all levels in one persistent launch over the flat pair list
+// (one global CSR sorted by (target, source)).  A CTA takes 128 consecutive
+// pairs, one per thread; every thread parks its b row in SMEM, then the CTA
+// folds each target segment in ascending pair order (one task per
+// coefficient and segment, coalesced row updates).  Targets wholly inside
+// the item are updated in place (exclusive owner, no atomics); targets whose
+// pairs span items leave ordered partials for k_m2l_fixup.
+constexpr int M2L_ITEM = 128;
+constexpr int PASCAL_N = 64;
+
+struct PascalTab {
+  double v[PASCAL_N][PASCAL_N];
+};
+constexpr PascalTab make_pascal() {
+  PascalTab t{};
+  unsigned long long row[PASCAL_N] = {};
+  for (int n = 0; n < PASCAL_N; ++n) {
+    for (int k = n; k >= 1; --k) row[k] += row[k - 1];   // C(n, k), exact in u64 for n < 64
+    row[0] = 1;
+    for (int k = 0; k < PASCAL_N; ++k) t.v[n][k] = k <= n ? (double)row[k] : 0.0;
+  }
+  return t;
+}
+__constant__ PascalTab c_pascal = make_pascal();
+
 template <int PM>
-__global__ void __launch_bounds__(128, M2L_MIN_BLOCKS)
-k_m2l(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
-      const int* __restrict__ w_tgt, const double* __restrict__ cx,
-      const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
-      double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
-  if (lists_overflowed(st)) return;
-  const long long npairs = *total_ptr;
-  const long long nitems = (npairs + 31) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long warps_total = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; item < nitems;
-       item += warps_total) {
-    const long long i = item * 32 + lane;
-    const bool valid = i < npairs;
-    const int t = valid ? w_tgt[i] : -1;
-    cplx c[PM + 1];
-    if (valid) {
-      const int s = w_src[i];
-      const cplx rho{cx[s] - cx[t], cy[s] - cy[t]};            // source - target
-      const bool sing = rho.x == 0.0 && rho.y == 0.0;
-      if (sing) atomicOr(&st->flags, ST_M2L_SINGULAR);
-      const cplx inv = sing ? cplx{0.0, 0.0} : crcp(rho);
-      const double2* a = mult + (long long)s * (p + 1);
-      // prescale c_{j-1} = a_j (-1)^j / rho^j  (operators.py:334-338)
-      cplx pw = inv;
-#pragma unroll
-      for (int k = 1; k <= PM; ++k) {
-        const cplx v = cmul(ld_coef(a, k, p), pw);
-        c[k - 1] = (k & 1) ? cplx{-v.x, -v.y} : v;
-        pw = cmul(pw, inv);
-      }
-      c[PM] = cplx{0.0, 0.0};
-      // pass 1, old-value slices (operators.py:339-341)
-#pragma unroll
-      for (int k = 2; k <= PM; ++k)
-#pragma unroll
-        for (int j = PM - k; j < PM; ++j) c[j] = cadd(c[j], c[j + 1]);
-      // pass 2, new-value cascade (operators.py:342-344)
-#pragma unroll
-      for (int k = PM; k >= 1; --k)
-#pragma unroll
-        for (int j = k; j <= PM; ++j) c[j] = cadd(c[j], c[j - 1]);
-      // postscale b_j = c_j / rho^j (operators.py:349-350)
-      pw = inv;
-#pragma unroll
-      for (int j = 1; j <= PM; ++j) {
-        c[j] = cmul(c[j], pw);
-        pw = cmul(pw, inv);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j <= PM; ++j) c[j] = cplx{0.0, 0.0};
-    }
-    // segmented inclusive scan over lanes keyed by target
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int tu = __shfl_up_sync(0xffffffffu, t, d);
-      const bool take = lane >= d && tu == t;
-#pragma unroll
-      for (int j = 0; j <= PM; ++j) {
-        const double ux = __shfl_up_sync(0xffffffffu, c[j].x, d);
-        const double uy = __shfl_up_sync(0xffffffffu, c[j].y, d);
-        if (take) { c[j].x += ux; c[j].y += uy; }
-      }
-    }
-    const int tn = __shfl_down_sync(0xffffffffu, t, 1);
-    const int t0 = __shfl_sync(0xffffffffu, t, 0);
-    bool seg_end;
-    bool ends_after = false;
-    if (lane == 31) {
-      ends_after = valid && i + 1 < npairs && w_tgt[i + 1] == t;
-      seg_end = valid;
-    } else {
-      seg_end = valid && tn != t;
-    }
-    if (seg_end) {
-      const bool starts_before = (t == t0) && item > 0 && w_tgt[item * 32 - 1] == t;
-      if (!starts_before && !ends_after) {
-        double2* dst = local + (long long)t * (p + 1);
-#pragma unroll
-        for (int j = 0; j <= PM; ++j)
-          if (j <= p) {
-            double2 v = dst[j];
-            dst[j] = make_double2(v.x + c[j].x, v.y + c[j].y);
-          }
-      } else {
-        const int slot = starts_before ? 0 : 1;
-        double2* dst = partials + (item * 2 + slot) * (p + 1);
-#pragma unroll
-        for (int j = 0; j <= PM; ++j)
-          if (j <= p) dst[j] = make_double2(c[j].x, c[j].y);
-        unsigned char f = starts_before ? (ends_after ? 5 : 1) : 2;
-        // first and last segment of one item are written by different lanes
-        atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)),
-                 (unsigned int)f << (8 * (item & 3)));
-      }
-    }
+struct M2LDenseCfg {
+  static constexpr int R = 2 * (PM + 1);          // SMEM rows (re/im per coefficient)
+  static constexpr int STR = M2L_ITEM + 1;        // odd row stride: conflict-free
+  static constexpr int SMEM = R * STR * 8;
+  static constexpr int MINB = PM <= 20 ? 4 : (PM <= 24 ? 3 : 2);
+};
+
+// one coalesced row update of a target segment's sum (coefficient j, part comp)
+__device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
+                                         unsigned char* item_flags, long long item, int p, int t,
+                                         int j, int comp, double v, bool starts_before,
+                                         bool ends_after) {
+  if (!starts_before && !ends_after) {
+    double* dst = reinterpret_cast<double*>(local + (long long)t * (p + 1)) + 2 * j + comp;
+    *dst += v;
+    return;
+  }
+  const int slot = starts_before ? 0 : 1;
+  reinterpret_cast<double*>(partials + (item * 2 + slot) * (p + 1))[2 * j + comp] = v;
+  if (j == 0 && comp == 0) {
+    const unsigned f = starts_before ? (ends_after ? 5u : 1u) : 2u;
+    atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)), f << (8 * (item & 3)));
   }
 }
 
-// Same M2L with a lane PAIR per interaction: the cascades are real-linear, so
-// lane 2i carries the real parts and lane 2i+1 the imaginary parts of pair i;
-// only the pre/post scalings mix them (one shuffle per coefficient).  Half
-// the registers of the thread-per-pair form, so twice the resident warps to
-// hide FP64 and L2 latency.  16 pairs per warp item.
+// the pair a thread owns in one item, with its source row prefetched
+template <int PM>
+struct M2LPair {
+  int t, s;
+  double2 a[PM];
+};
+
+template <int PM>
+__device__ __forceinline__ void m2l_load_pair(M2LPair<PM>& P, long long i, long long npairs,
+                                              const int* __restrict__ w_src,
+                                              const int* __restrict__ w_tgt,
+                                              const double2* __restrict__ mult, int p) {
+  const bool valid = i < npairs;
+  P.t = valid ? __ldg(w_tgt + i) : -1;
+  P.s = valid ? __ldg(w_src + i) : 0;
+  const double2* a = mult + (long long)P.s * (p + 1);
+#pragma unroll
+  for (int k = 1; k <= PM; ++k) P.a[k - 1] = k <= p ? a[k] : make_double2(0.0, 0.0);
+}
+
+template <int PM>
+__global__ void __launch_bounds__(M2L_ITEM, M2LDenseCfg<PM>::MINB)
+k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
+            const int* __restrict__ w_tgt, const double* __restrict__ cx,
+            const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
+            double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+  static_assert(2 * PM <= PASCAL_N, "Pascal table too small for this order");
+  using Cfg = M2LDenseCfg<PM>;
+  if (lists_overflowed(st)) return;
+  extern __shared__ double red[];                 // [R][STR]
+  __shared__ int s_t[M2L_ITEM];
+  __shared__ int s_seg[M2L_ITEM + 1];
+  __shared__ int s_nseg;
+  __shared__ int s_wcnt[M2L_ITEM / 32];
+  const long long npairs = *total_ptr;
+  const long long nitems = (npairs + M2L_ITEM - 1) / M2L_ITEM;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  M2LPair<PM> P;
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    m2l_load_pair<PM>(P, item * M2L_ITEM + tid, npairs, w_src, w_tgt, mult, p);
+    const bool valid = P.t >= 0;
+    const int t = P.t;
+    const int tt = valid ? t : 0;
+    const double rx = cx[P.s] - cx[tt], ry = cy[P.s] - cy[tt];   // source - target
+    const bool sing = valid && rx == 0.0 && ry == 0.0;
+    if (sing) atomicOr(&st->flags, ST_M2L_SINGULAR);
+    const cplx inv = (valid && !sing) ? crcp(cplx{rx, ry}) : cplx{0.0, 0.0};
+    // alpha_k = a_k q^k with q = -1/rho (operators.py:334-338)
+    const cplx q{-inv.x, -inv.y};
+    double ax[PM], ay[PM];
+    {
+      cplx pw = q;
+#pragma unroll
+      for (int k = 1; k <= PM; ++k) {
+        const cplx v = cmul(cplx{P.a[k - 1].x, P.a[k - 1].y}, pw);
+        ax[k - 1] = v.x;
+        ay[k - 1] = v.y;
+        pw = cmul(pw, q);
+      }
+    }
+    // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
+    {
+      cplx pw = inv;
+#pragma unroll
+      for (int j = 0; j <= PM; ++j) {
+        double sx = c_pascal.v[j][0] * ax[0], sy = c_pascal.v[j][0] * ay[0];
+#pragma unroll
+        for (int k = 2; k <= PM; ++k) {
+          sx = fma(c_pascal.v[j + k - 1][k - 1], ax[k - 1], sx);
+          sy = fma(c_pascal.v[j + k - 1][k - 1], ay[k - 1], sy);
+        }
+        cplx b{sx, sy};
+        if (j > 0) {
+          b = cmul(b, pw);
+          pw = cmul(pw, inv);
+        }
+        red[(2 * j) * Cfg::STR + tid] = b.x;
+        red[(2 * j + 1) * Cfg::STR + tid] = b.y;
+      }
+    }
+    s_t[tid] = t;
+    __syncthreads();
+    // segment starts (pairs are sorted by target)
+    const bool start = valid && (tid == 0 || s_t[tid - 1] != t);
+    const unsigned bal = __ballot_sync(0xffffffffu, start);
+    if (lane == 0) s_wcnt[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int w = 0; w < M2L_ITEM / 32; ++w) before += w < wid ? s_wcnt[w] : 0;
+    if (start) s_seg[before + __popc(bal & ((1u << lane) - 1))] = tid;
+    if (tid == M2L_ITEM - 1) {
+      int tot = 0;
+#pragma unroll
+      for (int w = 0; w < M2L_ITEM / 32; ++w) tot += s_wcnt[w];
+      s_nseg = tot;
+      s_seg[tot] = (int)min((long long)M2L_ITEM, npairs - item * M2L_ITEM);
+    }
+    __syncthreads();
+    const int nseg = s_nseg;
+    const int R = 2 * (p + 1);
+    const int t0 = s_t[0];
+    const bool first_cont = item > 0 && w_tgt[item * M2L_ITEM - 1] == t0;
+    const int nvalid = s_seg[nseg];
+    const long long last = item * M2L_ITEM + nvalid - 1;
+    const bool last_cont = last + 1 < npairs && w_tgt[last + 1] == s_t[nvalid - 1];
+    for (int task = tid; task < nseg * R; task += M2L_ITEM) {
+      const int sg = task / R, r = task - sg * R;
+      const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
+      const double* row = red + r * Cfg::STR;
+      // four interleaved chains (fixed order), then ((0+1)+(2+3))
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int q = q0;
+      for (; q + 4 <= q1; q += 4) {
+        a0 += row[q];
+        a1 += row[q + 1];
+        a2 += row[q + 2];
+        a3 += row[q + 3];
+      }
+      if (q < q1) a0 += row[q];
+      if (q + 1 < q1) a1 += row[q + 1];
+      if (q + 2 < q1) a2 += row[q + 2];
+      m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, (a0 + a1) + (a2 + a3),
+               sg == 0 && first_cont, sg == nseg - 1 && last_cont);
+    }
+    __syncthreads();
+  }
+}
+
 // Target-owned M2L (default).  One warp per target box walks the target's
 // weak list in chunks of 16 pairs; lane pair (2i, 2i+1) carries the real /
 // imaginary part of pair i (the cascades of operators.py:339-344 are
@@ -442,133 +525,6 @@ k_m2l_target(long long nbox, const int* __restrict__ woff, const int* __restrict
 #pragma unroll
     for (int j = 0; j <= PM; ++j)
       if (j <= p && (j & 15) == pl) row[2 * j + h] += acc[j];
-  }
-}
-
-// one coalesced row update of a target segment's sum (coefficient j, part comp)
-__device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
-                                         unsigned char* item_flags, long long item, int p, int t,
-                                         int j, int comp, double v, bool starts_before,
-                                         bool ends_after) {
-  if (!starts_before && !ends_after) {
-    double* dst = reinterpret_cast<double*>(local + (long long)t * (p + 1)) + 2 * j + comp;
-    *dst += v;
-    return;
-  }
-  const int slot = starts_before ? 0 : 1;
-  reinterpret_cast<double*>(partials + (item * 2 + slot) * (p + 1))[2 * j + comp] = v;
-  if (j == 0 && comp == 0) {
-    const unsigned f = starts_before ? (ends_after ? 5u : 1u) : 2u;
-    atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)), f << (8 * (item & 3)));
-  }
-}
-
-template <int PM>
-__global__ void __launch_bounds__(128)
-k_m2l_split(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
-            const int* __restrict__ w_tgt, const double* __restrict__ cx,
-            const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
-            double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
-  if (lists_overflowed(st)) return;
-  extern __shared__ double red[];          // 4 warps x 32 lanes x RS doubles
-  __shared__ int s_tgt[4][16];
-  constexpr int RS = (PM + 1) | 1;         // odd row stride: conflict-free 8-byte banks
-  const long long npairs = *total_ptr;
-  const long long nitems = (npairs + 15) >> 4;
-  const int lane = threadIdx.x & 31, h = lane & 1, pl = lane >> 1;
-  const long long warps_total = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; item < nitems;
-       item += warps_total) {
-    const long long i = item * 16 + pl;
-    const bool valid = i < npairs;
-    // padding lanes run the same code on box 0 with a zero reciprocal
-    const int t = valid ? w_tgt[i] : -1;
-    const int s = valid ? w_src[i] : 0;
-    const int tt = valid ? t : 0;
-    const cplx rho{cx[s] - cx[tt], cy[s] - cy[tt]};               // source - target
-    const bool sing = valid && rho.x == 0.0 && rho.y == 0.0;
-    if (__any_sync(0xffffffffu, sing) && lane == 0) atomicOr(&st->flags, ST_M2L_SINGULAR);
-    const cplx inv = (valid && !sing) ? crcp(rho) : cplx{0.0, 0.0};
-    // q = -1/rho: q^k = (-1)^k / rho^k.  The lane pair shares the power
-    // sequence: each lane advances its own component, the partner's comes by
-    // shuffle, so a complex power costs 2 FP64 ops per lane instead of 4.
-    const double qx = -inv.x, qy = -inv.y;
-    const double2* a = mult + (long long)s * (p + 1);
-    double c[PM + 1];
-    // lane-dependent choices as bit masks (a select on h would make the
-    // compiler unswitch the unrolled loops and serialise both lane halves)
-    const unsigned long long hm = h ? ~0ull : 0ull;            // all ones on the imag lane
-    const unsigned long long neg0 = h ? 0ull : 0x8000000000000000ull;
-    {
-      double own = dsel(qy, qx, hm);                               // component h of q^1
-#pragma unroll
-      for (int k = 1; k <= PM; ++k) {
-        const double part = __shfl_xor_sync(0xffffffffu, own, 1);
-        const double ps = dxor(part, neg0);                        // partner, signed
-        const cplx ak = ld_coef(a, k, p);
-        c[k - 1] = fma(ak.x, own, ak.y * ps);                      // (a_k q^k)_h
-        own = fma(ps, qy, own * qx);                               // (q^{k+1})_h
-      }
-      c[PM] = 0.0;
-    }
-#pragma unroll
-    for (int k = 2; k <= PM; ++k)                 // pass 1, old values (operators.py:339-341)
-#pragma unroll
-      for (int j = PM - k; j < PM; ++j) c[j] += c[j + 1];
-#pragma unroll
-    for (int k = PM; k >= 1; --k)                 // pass 2, new values (operators.py:342-344)
-#pragma unroll
-      for (int j = k; j <= PM; ++j) c[j] += c[j - 1];
-    {   // postscale b_j = c_j / rho^j = c_j (-q)^j (operators.py:349-350)
-      double own = dsel(qy, qx, hm);
-#pragma unroll
-      for (int j = 1; j <= PM; ++j) {
-        const double pp = __shfl_xor_sync(0xffffffffu, own, 1);    // partner of q^j
-        const double cp = __shfl_xor_sync(0xffffffffu, c[j], 1);   // partner of c_j
-        // (c q^j)_h  h=0: c_o w_o - c_p w_p ;  h=1: c_p w_o + c_o w_p
-        const double A = dsel(cp, c[j], hm);
-        const double B = dsel(c[j], dxor(cp, 0x8000000000000000ull), hm);
-        const double v = fma(A, own, B * pp);
-        c[j] = (j & 1) ? -v : v;
-        own = fma(dxor(pp, neg0), qy, own * qx);
-      }
-    }
-    // per-target sums through SMEM: every lane parks its row, then lane r
-    // owns coefficient r>>1 (component r&1) and walks the 16 pairs in order,
-    // emitting one coalesced row update per target segment
-    double* row = red + ((threadIdx.x >> 5) * 32 + lane) * RS;
-#pragma unroll
-    for (int j = 0; j <= PM; ++j) row[j] = c[j];
-    int* wt = s_tgt[threadIdx.x >> 5];
-    if (h == 0) wt[pl] = t;
-    const int t0 = __shfl_sync(0xffffffffu, t, 0);
-    const bool first_cont = item > 0 && t0 >= 0 && w_tgt[item * 16 - 1] == t0;
-    const long long last = min(item * 16 + 15, npairs - 1);
-    const int t_last = w_tgt[last];
-    const bool last_cont = last + 1 < npairs && w_tgt[last + 1] == t_last;
-    __syncwarp();
-    const double* wred = red + (threadIdx.x >> 5) * 32 * RS;
-    for (int r = lane; r < 2 * (p + 1); r += 32) {
-      const int j = r >> 1, comp = r & 1;
-      double acc = 0.0;
-      int seg_t = wt[0], seg_first = 1;
-      for (int q = 0; q < 16; ++q) {
-        const int tq = wt[q];
-        if (tq < 0) break;
-        if (tq != seg_t) {     // segment ends before pair q
-          m2l_emit(local, partials, item_flags, item, p, seg_t, j, comp, acc,
-                   seg_first && first_cont, false);
-          seg_t = tq;
-          seg_first = 0;
-          acc = 0.0;
-        }
-        acc += wred[(2 * q + comp) * RS + j];
-      }
-      if (seg_t >= 0)
-        m2l_emit(local, partials, item_flags, item, p, seg_t, j, comp, acc,
-                 seg_first && first_cont, last_cont);
-    }
-    __syncwarp();
   }
 }
 
@@ -679,52 +635,46 @@ struct Launch {
     const int L = T.L;
     if (L == 0) return;
     const int* total = Ls.weak_off.as<int>() + level_base(L + 1);
-    if (m2l_variant() == 2) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const long long nbox = level_base(L + 1);
-      const unsigned grid = (unsigned)std::min<long long>(nblk(nbox * 32, 128), 64ll * sms);
-      note_launch();
-      k_m2l_target<PM><<<grid, 128, 0, st>>>(nbox, Ls.weak_off.as<int>(), Ls.weak_idx.as<int>(),
-                                             T.box_cx.as<double>(), T.box_cy.as<double>(),
-                                             E.mult.as<double2>(), E.local.as<double2>(), E.p,
-                                             dstat);
-      return;
-    }
-    const bool split = m2l_variant() == 1;
-    const int item_pairs = split ? 16 : 32;
-    const long long items = (Ls.cap_weak + item_pairs - 1) / item_pairs;
-    E.partials.reserve(sizeof(double2) * 2 * items * (E.p + 1));
-    E.item_flags.reserve(((items + 4) & ~3ll) + 8);
-    FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = (unsigned)std::min<long long>(nblk(items * 32, 128), 32ll * sms);
-    note_launch();
-    if (split) {
-      constexpr int RS = (PM + 1) | 1;
-      const int smem = 128 * RS * (int)sizeof(double);
-      if (smem > 48 * 1024)
-        FMM_CUDA(cudaFuncSetAttribute(k_m2l_split<PM>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      k_m2l_split<PM><<<grid, 128, smem, st>>>(total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(),
-                                            T.box_cx.as<double>(), T.box_cy.as<double>(),
-                                            E.mult.as<double2>(), E.local.as<double2>(),
-                                            E.partials.as<double2>(),
-                                            E.item_flags.as<unsigned char>(), E.p, dstat);
+    if constexpr (2 * PM > PASCAL_N) {
+      launch_target(T, Ls, E, dstat, st);
     } else {
-      k_m2l<PM><<<grid, 128, 0, st>>>(total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(),
-                                      T.box_cx.as<double>(), T.box_cy.as<double>(),
-                                      E.mult.as<double2>(), E.local.as<double2>(),
-                                      E.partials.as<double2>(), E.item_flags.as<unsigned char>(),
-                                      E.p, dstat);
+      if (m2l_force_target()) {
+        launch_target(T, Ls, E, dstat, st);
+        return;
+      }
+      using Cfg = M2LDenseCfg<PM>;
+      const long long items = (Ls.cap_weak + M2L_ITEM - 1) / M2L_ITEM;
+      E.partials.reserve(sizeof(double2) * 2 * items * (E.p + 1));
+      E.item_flags.reserve(((items + 4) & ~3ll) + 8);
+      FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
+      static bool attr = false;
+      if (!attr) {
+        FMM_CUDA(cudaFuncSetAttribute(k_m2l_dense<PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::SMEM));
+        attr = true;
+      }
+      const unsigned grid = (unsigned)std::min<long long>(std::max(1ll, items),
+                                                          (long long)Cfg::MINB * sm_count());
+      note_launch();
+      k_m2l_dense<PM><<<grid, M2L_ITEM, Cfg::SMEM, st>>>(
+          total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
+          T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
+          E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
+      note_launch();
+      k_m2l_fixup<<<std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st>>>(
+          total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
+          E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, M2L_ITEM, dstat);
     }
+  }
+  static void launch_target(const TreeState& T, const ListState& Ls, ExpState& E,
+                            DevStatus* dstat, cudaStream_t st) {
+    const long long nbox = level_base(T.L + 1);
+    const unsigned grid = (unsigned)std::min<long long>(nblk(nbox * 32, 128), 64ll * sm_count());
     note_launch();
-    k_m2l_fixup<<<std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st>>>(
-        total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
-        E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, item_pairs, dstat);
+    k_m2l_target<PM><<<grid, 128, 0, st>>>(nbox, Ls.weak_off.as<int>(), Ls.weak_idx.as<int>(),
+                                           T.box_cx.as<double>(), T.box_cy.as<double>(),
+                                           E.mult.as<double2>(), E.local.as<double2>(), E.p,
+                                           dstat);
   }
   static void l2l(const TreeState& T, ExpState& E, cudaStream_t st) {
     for (int l = 1; l < T.L; ++l) {
