@@ -8,6 +8,7 @@ every engine call raises.  The library is built in-tree by
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -80,11 +81,13 @@ def load_library():
     global _lib
     with _lib_lock:
         if _lib is None:
-            if not LIB_PATH.exists():
+            # FMM2D_LIBRARY selects an alternative in-tree build (A/B measurements)
+            path = Path(os.environ.get("FMM2D_LIBRARY", str(LIB_PATH)))
+            if not path.exists():
                 raise RuntimeError(
-                    f"{LIB_PATH} is missing: build it with `python -m paper_1205_4611_b200._build` "
+                    f"{path} is missing: build it with `python -m paper_1205_4611_b200._build` "
                     "(the engine has no CPU fallback)")
-            lib = C.CDLL(str(LIB_PATH))
+            lib = C.CDLL(str(path))
             for name, (res, args) in _SIGS.items():
                 fn = getattr(lib, name)
                 fn.restype = res

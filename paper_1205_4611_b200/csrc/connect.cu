@@ -7,18 +7,19 @@
 // One warp per target box.  Candidates of box b are the children of the
 // boxes strongly coupled to its parent, generated in ascending order, so the
 // ballot/popc compaction below writes every list already sorted ascending
-// (the property connectivity.py:10-12 promises).  Counts -> device scan ->
-// fill; the weak lists of all levels form one global CSR (global box ids),
+// (the property connectivity.py:10-12 promises).  One launch per level:
+// predicates -> decoupled look-back offsets -> fill; the weak lists of all
+// levels form one global CSR (global box ids),
 // which is also the pair list the single M2L launch consumes.  No host sync:
 // list buffers are sized from capacities kept in the context, and a fill that
 // would overflow only raises ST_OVERFLOW (the host then regrows and reruns).
 #include "engine.h"
+#include "lookback.cuh"
 
 namespace fmm {
 
 namespace {
 
-constexpr int CONN_THREADS = 256;
 
 struct LevelGeo {
   const double* cx;
@@ -26,121 +27,283 @@ struct LevelGeo {
   const double* r;
 };
 
-// candidate c (0-based) of target b at level l: child (c & 3) of the (c >> 2)-th
-// strong box of b's parent
-__global__ void __launch_bounds__(CONN_THREADS)
+constexpr int CL_WARPS = 8;     // warps (= parents, or finest targets) per CTA
+constexpr int CL_MAXM = 32;     // ballot masks cached per target (1024 candidates)
+
+// One level of classify_level (connectivity.py:47-68) in ONE pass: a warp per
+// parent box evaluates its four children against the children of the
+// parent's strong list (the siblings share that candidate set, so each
+// candidate's geometry is loaded once for four predicates); the far/near
+// ballot masks stay in SMEM; a decoupled look-back gives every target its
+// offsets in the global weak CSR and in the level's strong CSR; the lists
+// are then written compacted, ascending.  A CTA that finds the lists already
+// overflowed publishes zero counts (never stalls its successors) and writes
+// nothing; overflowing writes are skipped and flagged for the host's regrow.
+__global__ void __launch_bounds__(CL_WARPS * 32)
 k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
-           const int* __restrict__ ps_idx, int* wcnt, int* scnt,
-           // fill mode (woff != nullptr)
-           const int* __restrict__ woff, int* widx, int* wtgt, long long wcap,
-           const int* __restrict__ soff, int* sidx, long long scap, DevStatus* st) {
-  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long nb = 1ll << (2 * l);
-  if (b >= nb || lists_overflowed(st)) return;
-  const long long gb = level_base(l) + b;
+           const int* __restrict__ ps_idx, int* so, int* sidx, long long scap, int* woff,
+           int* widx, int* wtgt, long long wcap, LookbackState lbs, unsigned ntiles,
+           DevStatus* st) {
+  __shared__ unsigned s_mask[CL_WARPS][4][CL_MAXM];
+  __shared__ int s_cnt[CL_WARPS][4][2];
+  __shared__ long long s_excl[2];
+  __shared__ unsigned s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
+  __syncthreads();
+  const unsigned tile = s_tile;
+  const long long np = 1ll << (2 * (l - 1));
+  const long long P = (long long)tile * CL_WARPS + w;
+  const bool dead = lists_overflowed(st);
+  const bool live = P < np && !dead;
   const long long lb = level_base(l);
-  const double rt = geo.r[gb], xt = geo.cx[gb], yt = geo.cy[gb];
-  const int a0 = ps_off[b >> 2], a1 = ps_off[(b >> 2) + 1];
-  const int ncand = 4 * (a1 - a0);
-  const bool fill = woff != nullptr;
-  long long wpos = 0, spos = 0;
-  if (fill) {
-    wpos = woff[gb];
-    spos = soff[b];
-    if (lane == 0) {
-      const long long wend = woff[gb + 1], send = soff[b + 1];
-      if (wend > wcap || send > scap) {
-        atomicOr(&st->flags, ST_OVERFLOW);
-        atomicOr(&st->overflow_where, 1);
-      }
-    }
-    if (woff[gb + 1] > wcap || soff[b + 1] > scap) return;
+  int a0 = 0, ncand = 0;
+  if (live) {
+    a0 = ps_off[P];
+    ncand = 4 * (ps_off[P + 1] - a0);
   }
-  int nw = 0, ns = 0;
+  double rt[4], xt[4], yt[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const long long gb = lb + 4 * (live ? P : 0) + j;
+    rt[j] = geo.r[gb];
+    xt[j] = geo.cx[gb];
+    yt[j] = geo.cy[gb];
+  }
+  int nw[4] = {0, 0, 0, 0}, ns[4] = {0, 0, 0, 0};
   for (int c0 = 0; c0 < ncand; c0 += 32) {
     const int c = c0 + lane;
-    bool valid = c < ncand, far = false;
-    int cand = 0;
-    if (valid) {
-      cand = 4 * ps_idx[a0 + (c >> 2)] + (c & 3);
-      const long long gc = lb + cand;
+    const bool valid = c < ncand;
+    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
+    const long long gc = lb + cand;
+    const double xc = geo.cx[gc], yc = geo.cy[gc], rc = geo.r[gc];
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
       // d = |c_target - c_source| (geometry.py:40), then the θ-test (:41)
-      const double d = numpy_cabs(xt - geo.cx[gc], yt - geo.cy[gc]);
-      far = well_separated(rt, geo.r[gc], d, theta);
+      const bool far = valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
+      const unsigned m = __ballot_sync(0xffffffffu, far);
+      if (lane == 0 && (c0 >> 5) < CL_MAXM) s_mask[w][j][c0 >> 5] = m;
+      nw[j] += __popc(m);
+      ns[j] += __popc(vm & ~m);
     }
-    const unsigned wm = __ballot_sync(0xffffffffu, valid && far);
-    const unsigned sm = __ballot_sync(0xffffffffu, valid && !far);
-    if (fill) {
-      const unsigned below = (1u << lane) - 1u;
-      if (valid && far) {
-        const long long o = wpos + nw + __popc(wm & below);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s_cnt[w][j][0] = nw[j];
+      s_cnt[w][j][1] = ns[j];
+    }
+  }
+  __syncthreads();
+  if (w == 0) {
+    long long agg[2] = {0, 0}, excl[2];
+    for (int q = 0; q < CL_WARPS; ++q)
+      for (int j = 0; j < 4; ++j) {
+        agg[0] += s_cnt[q][j][0];
+        agg[1] += s_cnt[q][j][1];
+      }
+    lb_prefix<2>(lbs, tile, agg, excl);
+    if (lane == 0) {
+      s_excl[0] = excl[0];
+      s_excl[1] = excl[1];
+    }
+  }
+  __syncthreads();
+  // out[0] may alias the base; it is rewritten with the same value, so racing reads agree
+  const long long wbase0 = woff[lb];
+  long long wb = wbase0 + s_excl[0], sb = s_excl[1];
+  for (int q = 0; q < w; ++q)
+    for (int j = 0; j < 4; ++j) {
+      wb += s_cnt[q][j][0];
+      sb += s_cnt[q][j][1];
+    }
+  long long wpos[4], spos[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    wpos[j] = wb;
+    spos[j] = sb;
+    wb += nw[j];
+    sb += ns[j];
+  }
+  if (P < np && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      so[4 * P + j] = (int)spos[j];
+      woff[lb + 4 * P + j] = (int)wpos[j];
+    }
+  }
+  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {   // totals: end of this level
+    long long wt = wbase0 + s_excl[0], stt = s_excl[1];
+    for (int q = 0; q < CL_WARPS; ++q)
+      for (int j = 0; j < 4; ++j) {
+        wt += s_cnt[q][j][0];
+        stt += s_cnt[q][j][1];
+      }
+    so[4 * np] = (int)stt;
+    woff[lb + 4 * np] = (int)wt;
+  }
+  if (!live) return;
+  if (wb > wcap || sb > scap) {
+    if (lane == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 1);
+    }
+    return;
+  }
+  const unsigned below = (1u << lane) - 1u;
+  for (int c0 = 0; c0 < ncand; c0 += 32) {
+    const int c = c0 + lane;
+    const bool valid = c < ncand;
+    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    double xc = 0.0, yc = 0.0, rc = 0.0;
+    if ((c0 >> 5) >= CL_MAXM) {
+      const long long gc = lb + cand;
+      xc = geo.cx[gc];
+      yc = geo.cy[gc];
+      rc = geo.r[gc];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      unsigned m;
+      if ((c0 >> 5) < CL_MAXM) {
+        m = s_mask[w][j][c0 >> 5];
+      } else {
+        const bool far =
+            valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
+        m = __ballot_sync(0xffffffffu, far);
+      }
+      const unsigned sm = vm & ~m;
+      const long long gb = lb + 4 * P + j;
+      if ((m >> lane) & 1u) {
+        const long long o = wpos[j] + __popc(m & below);
         widx[o] = (int)(lb + cand);
         wtgt[o] = (int)gb;
       }
-      if (valid && !far) sidx[spos + ns + __popc(sm & below)] = cand;
+      if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
+      wpos[j] += __popc(m);
+      spos[j] += __popc(sm);
     }
-    nw += __popc(wm);
-    ns += __popc(sm);
-  }
-  if (!fill && lane == 0) {
-    wcnt[b] = nw;
-    scnt[b] = ns;
   }
 }
 
-// finest reclassification with the radii exchanging roles (connectivity.py:71-96)
-__global__ void __launch_bounds__(CONN_THREADS)
+// reclassify_finest (connectivity.py:71-96) in one pass: a warp per finest
+// target, kinds cached as ballot masks, three-counter look-back, compacted
+// ascending p2p / p2l / m2p lists.
+__global__ void __launch_bounds__(CL_WARPS * 32)
 k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
-             const int* __restrict__ s_idx, int* c_p2p, int* c_p2l, int* c_m2p,
-             const int* __restrict__ o_p2p, int* i_p2p, long long cap_p2p,
-             const int* __restrict__ o_p2l, int* i_p2l, long long cap_p2l,
-             const int* __restrict__ o_m2p, int* i_m2p, long long cap_m2p, DevStatus* st) {
-  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+             const int* __restrict__ s_idx, int* o_p2p, int* i_p2p, long long cap_p2p,
+             int* o_p2l, int* i_p2l, long long cap_p2l, int* o_m2p, int* i_m2p,
+             long long cap_m2p, LookbackState lbs, unsigned ntiles, DevStatus* st) {
+  __shared__ unsigned s_mask[CL_WARPS][2][CL_MAXM];   // p2l, m2p masks (p2p = valid & ~both)
+  __shared__ int s_cnt[CL_WARPS][3];
+  __shared__ long long s_excl[3];
+  __shared__ unsigned s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
+  __syncthreads();
+  const unsigned tile = s_tile;
   const long long nb = 1ll << (2 * L);
-  if (b >= nb || lists_overflowed(st)) return;
+  const long long b = (long long)tile * CL_WARPS + w;
+  const bool live = b < nb && !lists_overflowed(st);
   const long long lb = level_base(L);
-  const double rt = geo.r[lb + b], xt = geo.cx[lb + b], yt = geo.cy[lb + b];
-  const int a0 = s_off[b], a1 = s_off[b + 1];
-  const bool fill = o_p2p != nullptr;
-  long long p0 = 0, l0 = 0, m0 = 0;
-  if (fill) {
-    if (o_p2p[b + 1] > cap_p2p || o_p2l[b + 1] > cap_p2l || o_m2p[b + 1] > cap_m2p) {
-      if (lane == 0) {
-        atomicOr(&st->flags, ST_OVERFLOW);
-        atomicOr(&st->overflow_where, 2);
-      }
-      return;
-    }
-    p0 = o_p2p[b]; l0 = o_p2l[b]; m0 = o_m2p[b];
+  int a0 = 0, a1 = 0;
+  if (live) {
+    a0 = s_off[b];
+    a1 = s_off[b + 1];
   }
-  int np = 0, nl = 0, nm = 0;
-  for (int c0 = a0; c0 < a1; c0 += 32) {
-    const int c = c0 + lane;
+  const long long gt = lb + (live ? b : 0);
+  const double rt = geo.r[gt], xt = geo.cx[gt], yt = geo.cy[gt];
+  auto kinds = [&](int c, unsigned& ml, unsigned& mm, unsigned& vm, int& src) {
     const bool valid = c < a1;
-    int src = 0, kind = 0;   // 0 p2p, 1 p2l (larger source), 2 m2p (smaller source)
+    int kind = 0;   // 0 p2p, 1 p2l (larger source), 2 m2p (smaller source)
+    src = valid ? s_idx[c] : 0;
     if (valid) {
-      src = s_idx[c];
       const double rs = geo.r[lb + src];
       const double d = numpy_cabs(xt - geo.cx[lb + src], yt - geo.cy[lb + src]);
       const bool sw = well_separated_swapped(rt, rs, d, theta);
       const bool moved = sw && src != b && rs != rt;
       kind = moved ? (rs > rt ? 1 : 2) : 0;
     }
-    const unsigned mp = __ballot_sync(0xffffffffu, valid && kind == 0);
-    const unsigned ml = __ballot_sync(0xffffffffu, valid && kind == 1);
-    const unsigned mm = __ballot_sync(0xffffffffu, valid && kind == 2);
-    if (fill && valid) {
-      const unsigned below = (1u << lane) - 1u;
-      if (kind == 0) i_p2p[p0 + np + __popc(mp & below)] = src;
-      else if (kind == 1) i_p2l[l0 + nl + __popc(ml & below)] = src;
-      else i_m2p[m0 + nm + __popc(mm & below)] = src;
+    vm = __ballot_sync(0xffffffffu, valid);
+    ml = __ballot_sync(0xffffffffu, kind == 1);
+    mm = __ballot_sync(0xffffffffu, kind == 2);
+  };
+  int n0 = 0, n1 = 0, n2 = 0;
+  for (int c0 = a0; c0 < a1; c0 += 32) {
+    unsigned ml, mm, vm;
+    int src;
+    kinds(c0 + lane, ml, mm, vm, src);
+    const int ch = (c0 - a0) >> 5;
+    if (lane == 0 && ch < CL_MAXM) {
+      s_mask[w][0][ch] = ml;
+      s_mask[w][1][ch] = mm;
     }
-    np += __popc(mp); nl += __popc(ml); nm += __popc(mm);
+    n0 += __popc(vm & ~(ml | mm));
+    n1 += __popc(ml);
+    n2 += __popc(mm);
   }
-  if (!fill && lane == 0) {
-    c_p2p[b] = np; c_p2l[b] = nl; c_m2p[b] = nm;
+  if (lane == 0) {
+    s_cnt[w][0] = n0;
+    s_cnt[w][1] = n1;
+    s_cnt[w][2] = n2;
+  }
+  __syncthreads();
+  if (w == 0) {
+    long long agg[3] = {0, 0, 0}, excl[3];
+    for (int q = 0; q < CL_WARPS; ++q)
+      for (int k = 0; k < 3; ++k) agg[k] += s_cnt[q][k];
+    lb_prefix<3>(lbs, tile, agg, excl);
+    if (lane == 0)
+      for (int k = 0; k < 3; ++k) s_excl[k] = excl[k];
+  }
+  __syncthreads();
+  long long pos[3] = {s_excl[0], s_excl[1], s_excl[2]};
+  for (int q = 0; q < w; ++q)
+    for (int k = 0; k < 3; ++k) pos[k] += s_cnt[q][k];
+  if (b < nb && lane == 0) {
+    o_p2p[b] = (int)pos[0];
+    o_p2l[b] = (int)pos[1];
+    o_m2p[b] = (int)pos[2];
+  }
+  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {
+    long long tot[3] = {s_excl[0], s_excl[1], s_excl[2]};
+    for (int q = 0; q < CL_WARPS; ++q)
+      for (int k = 0; k < 3; ++k) tot[k] += s_cnt[q][k];
+    o_p2p[nb] = (int)tot[0];
+    o_p2l[nb] = (int)tot[1];
+    o_m2p[nb] = (int)tot[2];
+  }
+  if (!live) return;
+  if (pos[0] + n0 > cap_p2p || pos[1] + n1 > cap_p2l || pos[2] + n2 > cap_m2p) {
+    if (lane == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 2);
+    }
+    return;
+  }
+  const unsigned below = (1u << lane) - 1u;
+  for (int c0 = a0; c0 < a1; c0 += 32) {
+    unsigned ml, mm, vm;
+    int src;
+    const int ch = (c0 - a0) >> 5;
+    if (ch < CL_MAXM) {
+      const int c = c0 + lane;
+      src = c < a1 ? s_idx[c] : 0;
+      vm = __ballot_sync(0xffffffffu, c < a1);
+      ml = s_mask[w][0][ch];
+      mm = s_mask[w][1][ch];
+    } else {
+      kinds(c0 + lane, ml, mm, vm, src);
+    }
+    const unsigned mp = vm & ~(ml | mm);
+    if ((mp >> lane) & 1u) i_p2p[pos[0] + __popc(mp & below)] = src;
+    if ((ml >> lane) & 1u) i_p2l[pos[1] + __popc(ml & below)] = src;
+    if ((mm >> lane) & 1u) i_m2p[pos[2] + __popc(mm & below)] = src;
+    pos[0] += __popc(mp);
+    pos[1] += __popc(ml);
+    pos[2] += __popc(mm);
   }
 }
 
@@ -215,12 +378,29 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     Ls.s_off[q].reserve(sizeof(int) * (nleaf + 1));
     Ls.s_idx[q].reserve(sizeof(int) * std::max<long long>(Ls.cap_strong, 1));
   }
-  for (DBuf* b : {&Ls.cnt_a, &Ls.cnt_b, &Ls.cnt_c}) b->reserve(sizeof(int) * nleaf);
   for (DBuf* b : {&Ls.p2p_off, &Ls.p2l_off, &Ls.m2p_off}) b->reserve(sizeof(int) * (nleaf + 1));
   Ls.p2p_idx.reserve(sizeof(int) * Ls.cap_p2p);
   Ls.p2l_idx.reserve(sizeof(int) * Ls.cap_p2l);
   Ls.m2p_idx.reserve(sizeof(int) * Ls.cap_m2p);
   Ls.hist.reserve(sizeof(int) * 4 * HIST_BINS);
+
+  // look-back state: flags + 3 counters per tile, grow-only, epoch-tagged
+  const long long max_tiles = (nleaf + CL_WARPS - 1) / CL_WARPS + 1;
+  if (Ls.lb_tiles < max_tiles) {
+    Ls.lb_flags.reserve(sizeof(unsigned) * max_tiles);
+    Ls.lb_vals.reserve(sizeof(long long) * 6 * max_tiles);
+    Ls.lb_ticket.reserve(sizeof(unsigned) * 4);
+    FMM_CUDA(cudaMemsetAsync(Ls.lb_flags.p, 0, sizeof(unsigned) * max_tiles, st));
+    FMM_CUDA(cudaMemsetAsync(Ls.lb_ticket.p, 0, sizeof(unsigned) * 4, st));
+    Ls.lb_tiles = max_tiles;
+  }
+  auto lbstate = [&]() {
+    Ls.lb_epoch = (Ls.lb_epoch + 1) & 0x3fffffffu;
+    if (Ls.lb_epoch == 0) Ls.lb_epoch = 1;
+    long long* v = Ls.lb_vals.as<long long>();
+    return LookbackState{Ls.lb_flags.as<unsigned>(), v, v + 3 * max_tiles,
+                         Ls.lb_ticket.as<unsigned>(), Ls.lb_epoch};
+  };
 
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
   int* woff = Ls.weak_off.as<int>();
@@ -228,45 +408,23 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   k_root_lists<<<1, 1, 0, st>>>(woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
-    const long long nb = 1ll << (2 * l);
-    const unsigned blocks = nblk(nb * 32, CONN_THREADS);
-    const int* ps_off = Ls.s_off[cur].as<int>();
-    const int* ps_idx = Ls.s_idx[cur].as<int>();
-    int* wcnt = Ls.cnt_a.as<int>();
-    int* scnt = Ls.cnt_b.as<int>();
+    const long long np = 1ll << (2 * (l - 1));
+    const unsigned ntiles = (unsigned)((np + CL_WARPS - 1) / CL_WARPS);
     note_launch();
-    k_classify<<<blocks, CONN_THREADS, 0, st>>>(l, geo, theta, ps_off, ps_idx, wcnt, scnt,
-                                                nullptr, nullptr, nullptr, 0, nullptr, nullptr,
-                                                0, dstat);
-    // weak offsets continue the global CSR: base = end of the previous level
-    int* wo = woff + level_base(l);
-    scan_exclusive(wcnt, wo, nb, Ls.totals, st, wo);
-    int* so = Ls.s_off[1 - cur].as<int>();
-    scan_exclusive(scnt, so, nb, Ls.totals, st, nullptr);
-    note_launch();
-    k_classify<<<blocks, CONN_THREADS, 0, st>>>(l, geo, theta, ps_off, ps_idx, nullptr, nullptr,
-                                                woff, Ls.weak_idx.as<int>(),
-                                                Ls.weak_tgt.as<int>(), Ls.cap_weak, so,
-                                                Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong,
-                                                dstat);
+    k_classify<<<ntiles, CL_WARPS * 32, 0, st>>>(
+        l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
+        Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
+        Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, dstat);
     cur = 1 - cur;
   }
   {
-    const unsigned blocks = nblk(nleaf * 32, CONN_THREADS);
-    const int* s_off = Ls.s_off[cur].as<int>();
-    const int* s_idx = Ls.s_idx[cur].as<int>();
+    const unsigned ntiles = (unsigned)((nleaf + CL_WARPS - 1) / CL_WARPS);
     note_launch();
-    k_reclassify<<<blocks, CONN_THREADS, 0, st>>>(
-        L, geo, theta, s_off, s_idx, Ls.cnt_a.as<int>(), Ls.cnt_b.as<int>(), Ls.cnt_c.as<int>(),
-        nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, dstat);
-    scan_exclusive(Ls.cnt_a.as<int>(), Ls.p2p_off.as<int>(), nleaf, Ls.totals, st);
-    scan_exclusive(Ls.cnt_b.as<int>(), Ls.p2l_off.as<int>(), nleaf, Ls.totals, st);
-    scan_exclusive(Ls.cnt_c.as<int>(), Ls.m2p_off.as<int>(), nleaf, Ls.totals, st);
-    note_launch();
-    k_reclassify<<<blocks, CONN_THREADS, 0, st>>>(
-        L, geo, theta, s_off, s_idx, nullptr, nullptr, nullptr, Ls.p2p_off.as<int>(),
+    k_reclassify<<<ntiles, CL_WARPS * 32, 0, st>>>(
+        L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),
         Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
-        Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, dstat);
+        Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles,
+        dstat);
   }
 }
 

@@ -22,6 +22,7 @@ constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
 
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -34,19 +35,42 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-// 1/r2 to ~1 ulp: MUFU reciprocal seed + two Newton steps on the FP64 pipe
+// 1/x for x > 0 to ~1 ulp: MUFU.RCP64H seed (~23 bits), then one cubic
+// Newton step y(1 + e + e^2), e = 1 - x y  (3 DFMA; error ~ e^3)
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
+  const double e = fma(-x, y, 1.0);
+  return fma(fma(e, e, e), y, y);
+}
+
+// One near-field interaction of source (z, g) with target y.  Exact
+// coincidence (r2 == 0, hence dx == dy == 0) contributes nothing and is
+// counted (operators.py:403-414); it is detected on the bit pattern of r2
+// and handled by evaluating 1/1 instead of 1/0, so the loop has no branch
+// and no FP64 compare: g * 1 * dx = 0 exactly.
+__device__ __forceinline__ void p2p_term(double zx, double zy, double g, double yx, double yy,
+                                         double& bx, double& by, int& skips) {
+  const double dx = zx - yx, dy = zy - yy;
+  double r2 = fma(dx, dx, dy * dy);
+  const long long bits = __double_as_longlong(r2);
+  const bool zero = bits == 0;
+  skips += zero;
+  r2 = zero ? 1.0 : r2;
+  const double gs = g * rcp_nr(r2);
+  bx = fma(gs, dx, bx);
+  by = fma(gs, dy, by);
 }
 
 // One warp per target leaf.  The leaf's near sources (the concatenated source
 // ranges of its p2p boxes, ascending) are staged into a per-warp SMEM buffer
-// with cp.async, then every lane streams them from SMEM (broadcast reads).
+// with cp.async; the box table (ids, ranges, running offsets) is fetched once
+// per 32 boxes with coalesced loads and walked by shuffles, so staging costs
+// no dependent global round trips per box.  With n_e points in the current
+// block of <= 32, G = 32/n_e lane groups share each point; group k sums a
+// CONTIGUOUS slice of the staged sources (immediate-offset SMEM reads,
+// 4-way unrolled, two accumulator pairs), then the G partial sums are folded
+// in fixed lane order -- deterministic, no atomics on values.
 __global__ void __launch_bounds__(P2P_THREADS)
 k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
       const int* __restrict__ n_off, const int* __restrict__ n_idx,
@@ -63,67 +87,77 @@ k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
   const int q0 = n_off[b], q1 = n_off[b + 1];
   double2* sp = s_pos[w];
   double* sg = s_g[w];
-  unsigned long long skips = 0;
+  int skips = 0;
   for (int eb = e0; eb < e1; eb += 32) {
     const int ne = min(32, e1 - eb);
     const int G = 32 / ne;
     const bool active = lane < G * ne;
-    const int ei = lane % ne, grp = lane / ne;
-    double ax = 0.0, ay = 0.0;
+    const int ei = lane % ne, grp = active ? lane / ne : 0;
     const double2 y = eval_pos[eb + ei];
-    int q = q0, in_box = 0;
-    while (q < q1) {
-      // stage the next chunk of the concatenated near-source list
+    double ax = 0.0, ay = 0.0;
+    // walk the near boxes 32 at a time; (qb, ib) = next box and offset inside it
+    int qb = q0, ib = 0;
+    while (qb < q1) {
       int fill = 0;
-      while (q < q1 && fill < P2P_CHUNK) {
-        const int a = n_idx[q];
-        const int s0 = soff[a] + in_box, s1 = soff[a + 1];
-        const int take = min(s1 - s0, P2P_CHUNK - fill);
-        for (int t = lane; t < take; t += 32) {
-          cp_async16(sp + fill + t, src_pos + s0 + t);
-          cp_async8(sg + fill + t, src_g + s0 + t);
+      bool partial = false;
+      while (qb < q1 && fill < P2P_CHUNK && !partial) {
+        const int nq = min(32, q1 - qb);
+        int bs0 = 0, bcnt = 0;
+        if (lane < nq) {
+          const int a = n_idx[qb + lane];
+          bs0 = soff[a];
+          bcnt = soff[a + 1] - bs0;
         }
-        fill += take;
-        if (s0 + take == s1) { ++q; in_box = 0; } else { in_box += take; }
+        int k = 0;
+        for (; k < nq && fill < P2P_CHUNK; ++k) {
+          const int skip = k == 0 ? ib : 0;
+          const int s0 = __shfl_sync(0xffffffffu, bs0, k) + skip;
+          const int cnt = __shfl_sync(0xffffffffu, bcnt, k) - skip;
+          const int take = min(cnt, P2P_CHUNK - fill);
+          for (int t = lane; t < take; t += 32) {
+            cp_async16(sp + fill + t, src_pos + s0 + t);
+            cp_async8(sg + fill + t, src_g + s0 + t);
+          }
+          fill += take;
+          if (take < cnt) {          // chunk full inside box k: resume there next round
+            ib = skip + take;
+            partial = true;
+            break;
+          }
+        }
+        qb += k;
+        if (!partial) ib = 0;
       }
       cp_async_wait_all();
       __syncwarp();
       if (active) {
-        // four independent accumulator chains (fixed order, deterministic)
-        double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
-        int j = grp;
-        for (; j + 3 * G < fill; j += 4 * G) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double2 z = sp[j + u * G];
-            const double dx = z.x - y.x, dy = z.y - y.y;
-            const double r2 = fma(dx, dx, dy * dy);
-            const bool coincide = r2 == 0.0;
-            skips += coincide;
-            const double gs = coincide ? 0.0 : sg[j + u * G] * rcp_nr(r2);
-            bx[u] = fma(gs, dx, bx[u]);
-            by[u] = fma(gs, dy, by[u]);
-          }
+        const int j0 = fill * grp / G, j1 = fill * (grp + 1) / G;
+        const double2* zp = sp + j0;
+        const double* gp = sg + j0;
+        const int n = j1 - j0;
+        double bx0 = 0.0, by0 = 0.0, bx1 = 0.0, by1 = 0.0;
+        int j = 0;
+        for (; j + 4 <= n; j += 4) {
+          const double2 z0 = zp[j], z1 = zp[j + 1], z2 = zp[j + 2], z3 = zp[j + 3];
+          const double g0 = gp[j], g1 = gp[j + 1], g2 = gp[j + 2], g3 = gp[j + 3];
+          p2p_term(z0.x, z0.y, g0, y.x, y.y, bx0, by0, skips);
+          p2p_term(z1.x, z1.y, g1, y.x, y.y, bx1, by1, skips);
+          p2p_term(z2.x, z2.y, g2, y.x, y.y, bx0, by0, skips);
+          p2p_term(z3.x, z3.y, g3, y.x, y.y, bx1, by1, skips);
         }
-        for (; j < fill; j += G) {
-          const double2 z = sp[j];
-          const double dx = z.x - y.x, dy = z.y - y.y;
-          const double r2 = fma(dx, dx, dy * dy);
-          const bool coincide = r2 == 0.0;
-          skips += coincide;
-          const double gs = coincide ? 0.0 : sg[j] * rcp_nr(r2);
-          bx[0] = fma(gs, dx, bx[0]);
-          by[0] = fma(gs, dy, by[0]);
+        for (; j < n; ++j) {
+          const double2 z = zp[j];
+          p2p_term(z.x, z.y, gp[j], y.x, y.y, bx0, by0, skips);
         }
-        ax += (bx[0] + bx[1]) + (bx[2] + bx[3]);
-        ay += (by[0] + by[1]) + (by[2] + by[3]);
+        ax += bx0 + bx1;
+        ay += by0 + by1;
       }
       __syncwarp();
     }
     // fold the G lane groups of every point in fixed order
-    for (int q = 1; q < G; ++q) {
-      const double ox = __shfl_sync(0xffffffffu, ax, lane + q * ne);
-      const double oy = __shfl_sync(0xffffffffu, ay, lane + q * ne);
+    for (int k = 1; k < G; ++k) {
+      const double ox = __shfl_sync(0xffffffffu, ax, lane + k * ne);
+      const double oy = __shfl_sync(0xffffffffu, ay, lane + k * ne);
       if (grp == 0) { ax += ox; ay += oy; }
     }
     if (active && grp == 0) {
@@ -133,7 +167,7 @@ k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
     }
   }
   for (int d = 16; d; d >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, d);
-  if (lane == 0 && skips) atomicAdd(&st->p2p_skips, skips);
+  if (lane == 0 && skips) atomicAdd(&st->p2p_skips, (unsigned long long)skips);
 }
 
 // all-pairs direct sum, asymmetric mode: thread per target, SMEM source tiles
