@@ -21,6 +21,7 @@ enum : int {
   ST_M2P_SINGULAR = 8,    // operators.py:376-377
   ST_OVERFLOW = 16,       // a list buffer was too small: host regrows + reruns
   ST_RANK_RETRY = 32,     // a run of equal 32-bit rank keys was too long: rerun exact
+  ST_EVAL_TIES = 64,      // a coordinate tie straddles a cut: aliased evals need their own split
 };
 
 struct DevStatus {
@@ -60,6 +61,36 @@ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cplx{a.x * s, 
 // 1/z in real arithmetic (conjugate over squared modulus); caller guarantees z != 0
 __device__ __forceinline__ cplx crcp(cplx z) {
   double s = 1.0 / fma(z.x, z.x, z.y * z.y);
+  return cplx{z.x * s, -z.y * s};
+}
+
+// leaf (segment after S median halvings, tree.py:308-310) holding tree-order
+// position i of n: the source offsets are data independent (left = ceil(n/2))
+__device__ __forceinline__ long long leaf_of_position(long long i, long long n, int S) {
+  long long seg = 0, s0 = 0, cnt = n;
+  for (int s = 0; s < S; ++s) {
+    const long long k = (cnt + 1) >> 1;
+    if (i < s0 + k) {
+      seg = 2 * seg;
+      cnt = k;
+    } else {
+      seg = 2 * seg + 1;
+      s0 += k;
+      cnt -= k;
+    }
+  }
+  return seg;
+}
+
+// 1/z to ~1 ulp without an IEEE division: MUFU seed + one cubic Newton step
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(fma(e, e, e), y, y);
+}
+__device__ __forceinline__ cplx crcp_fast(cplx z) {
+  const double s = rcp_fast(fma(z.x, z.x, z.y * z.y));
   return cplx{z.x * s, -z.y * s};
 }
 

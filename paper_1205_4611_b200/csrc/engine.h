@@ -68,7 +68,15 @@ struct TreeState {
   DBuf src_pos, src_g, src_perm;     // double2, double, int32
   DBuf eval_pos, eval_perm;          // double2, int32
   DBuf eval_leaf_off;                // int32[4^L + 1]
-  const unsigned* eval_leaf = nullptr;  // leaf of each tree-ordered eval point (L > 0)
+  bool eval_full = false;            // aliased evals take the full descend path (cut ties)
+  // tree-ordered evaluation points as the consumers see them: the owned
+  // buffers above, or -- aliased evaluation points with no coordinate tie at
+  // any cut -- the source arrays themselves (identical partition)
+  const double2* epos_t = nullptr;
+  const int* eperm_t = nullptr;
+  const int* eoff_t = nullptr;
+  const unsigned* eleaf_t = nullptr; // leaf of every tree-ordered eval point (separate evals;
+                                     // aliased ones derive it from the source offsets)
   DBuf box_cx, box_cy, box_hw, box_hh, box_r;  // all levels, global box id
   DBuf bbox;                         // double[4] + scratch
 };

@@ -122,7 +122,7 @@ k_p2l(int L, const int* __restrict__ offL, const int* __restrict__ l_off,
         atomicOr(&st->flags, ST_P2L_SINGULAR);
         continue;
       }
-      const cplx inv = crcp(d);
+      const cplx inv = crcp_fast(d);
       cplx w = cscale(inv, src_g[i]);
 #pragma unroll
       for (int k = 0; k <= PM; ++k) {
@@ -360,7 +360,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
     const double rx = cx[P.s] - cx[tt], ry = cy[P.s] - cy[tt];   // source - target
     const bool sing = valid && rx == 0.0 && ry == 0.0;
     if (sing) atomicOr(&st->flags, ST_M2L_SINGULAR);
-    const cplx inv = (valid && !sing) ? crcp(cplx{rx, ry}) : cplx{0.0, 0.0};
+    const cplx inv = (valid && !sing) ? crcp_fast(cplx{rx, ry}) : cplx{0.0, 0.0};
     // alpha_k = a_k q^k with q = -1/rho (operators.py:334-338)
     const cplx q{-inv.x, -inv.y};
     double ax[PM], ay[PM];
@@ -559,13 +559,15 @@ __global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __rest
 }
 
 // --------------------------------------------------------------------------
-// L2P + M2P (engine.py:132-160): one thread per evaluation point (tree order),
-// its leaf from the tree build.  phi = L2P (Horner in y - z0), then += each
-// m2p source in ascending order (operators.py:358-386).  Coefficients stream
-// from L1/L2 (the points of one leaf share them), so no register arrays.
+// L2P + M2P (engine.py:132-160): one thread per evaluation point (tree order);
+// its leaf comes from the eval tree (separate points) or, for points aliasing
+// the sources, from the data-independent source offsets.  phi = L2P (Horner
+// in y - z0), then += each m2p source in ascending order (operators.py:
+// 358-386).  Coefficient rows stream from L1/L2 (the points of one leaf
+// share them), all loads of a row in flight at once.
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_l2p_m2p(long long m, int L, const unsigned* __restrict__ leaf,
+k_l2p_m2p(long long m, int L, const unsigned* __restrict__ eleaf,
           const double2* __restrict__ eval_pos, const int* __restrict__ m_off,
           const int* __restrict__ m_idx, const double* __restrict__ cx,
           const double* __restrict__ cy, const double2* __restrict__ mult,
@@ -573,13 +575,13 @@ k_l2p_m2p(long long m, int L, const unsigned* __restrict__ leaf,
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= m || lists_overflowed(st)) return;
   const long long lb = level_base(L);
-  const long long b = leaf[e];
+  const long long b = eleaf ? (long long)eleaf[e] : leaf_of_position(e, m, 2 * L);
   const double2 y = eval_pos[e];
   const cplx w{y.x - cx[lb + b], y.y - cy[lb + b]};
   const double2* bl = local + (lb + b) * (p + 1);
   cplx c[PM + 1];
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) c[j] = ld_coef(bl, j, p);   // all loads in flight at once
+  for (int j = 0; j <= PM; ++j) c[j] = ld_coef(bl, j, p);
   cplx acc = c[PM];
 #pragma unroll
   for (int j = PM - 1; j >= 0; --j) acc = cadd(cmul(acc, w), c[j]);
@@ -590,7 +592,7 @@ k_l2p_m2p(long long m, int L, const unsigned* __restrict__ leaf,
       atomicOr(&st->flags, ST_M2P_SINGULAR);
       continue;
     }
-    const cplx inv = crcp(u);
+    const cplx inv = crcp_fast(u);
     const double2* a = mult + ga * (p + 1);
 #pragma unroll
     for (int j = 1; j <= PM; ++j) c[j] = ld_coef(a, j, p);
@@ -729,9 +731,9 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
   dispatch_p(E.p, [&](auto pm) {
     note_launch();
     k_l2p_m2p<decltype(pm)::value><<<nblk(T.m, 128), 128, 0, st>>>(
-        T.m, T.L, T.eval_leaf, T.eval_pos.as<double2>(), Ls.m2p_off.as<int>(),
-        Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
-        E.mult.as<double2>(), E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
+        T.m, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
+        T.box_cx.as<double>(), T.box_cy.as<double>(), E.mult.as<double2>(),
+        E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
   });
 }
 

@@ -257,6 +257,10 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
       T.exact_keys = true;
       continue;
     }
+    if ((s.flags & ST_EVAL_TIES) && T.aliased && !T.eval_full) {
+      T.eval_full = true;             // a coordinate tie at a cut: evals need their own split
+      continue;
+    }
     if ((s.flags & ST_DEGENERATE)) raise_degenerate(c);
     if (s.flags & ST_OVERFLOW) {
       if (attempt >= 8) throw ApiError{FMM2D_ECUDA, "interaction-list capacity did not converge"};
@@ -276,6 +280,7 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     }
     break;
   }
+  T.eval_full = false;                // next call starts on the aliased fast path again
   c->have_tree = c->have_lists = c->have_eval = true;
   c->theta = theta;
   const DevStatus& s = *c->h_status;
@@ -396,15 +401,22 @@ int fmm2d_build_tree(fmm2d_ctx* c, int64_t n, const double* pos, const double* g
     FMM_CUDA(cudaSetDevice(c->device));
     int64_t h2d = 0;
     set_inputs(c, n, pos, g, m, epos, false, &h2d);
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
       reset_status(c);
       build_tree_impl(c, nd);
       fetch_status(c);
       FMM_CUDA(cudaStreamSynchronize(c->st));
       FMM_CUDA(cudaGetLastError());
-      if (!(c->h_status->flags & ST_RANK_RETRY)) break;
-      c->T.exact_keys = true;
+      const int fl = c->h_status->flags;
+      if (fl & ST_RANK_RETRY) {
+        c->T.exact_keys = true;
+      } else if ((fl & ST_EVAL_TIES) && c->T.aliased && !c->T.eval_full) {
+        c->T.eval_full = true;
+      } else {
+        break;
+      }
     }
+    c->T.eval_full = false;
     c->have_tree = true;
     c->have_lists = c->have_eval = false;
     if (c->h_status->flags & ST_DEGENERATE) raise_degenerate(c);
@@ -447,7 +459,7 @@ int fmm2d_export_tree(fmm2d_ctx* c, double* center_xy, double* hw, double* hh,
       std::vector<int> so(off_base(2 * L + 1)), eo(nleaf + 1);
       FMM_CUDA(cudaMemcpy(so.data(), c->plan.d_off.p, sizeof(int) * so.size(),
                           cudaMemcpyDeviceToHost));
-      FMM_CUDA(cudaMemcpy(eo.data(), T.eval_leaf_off.p, sizeof(int) * (nleaf + 1),
+      FMM_CUDA(cudaMemcpy(eo.data(), T.eoff_t, sizeof(int) * (nleaf + 1),
                           cudaMemcpyDeviceToHost));
       long long w = 0;
       for (int l = 0; l <= L; ++l) {
@@ -465,12 +477,16 @@ int fmm2d_export_tree(fmm2d_ctx* c, double* center_xy, double* hw, double* hh,
       for (long long i = 0; i < cnt; ++i) dst[i] = t[i];
     };
     if (src_perm) copy_idx(src_perm, T.src_perm, T.n);
-    if (eval_perm) copy_idx(eval_perm, T.eval_perm, T.m);
+    if (eval_perm) {
+      std::vector<int> t(T.m);
+      FMM_CUDA(cudaMemcpy(t.data(), T.eperm_t, sizeof(int) * T.m, cudaMemcpyDeviceToHost));
+      for (long long i = 0; i < T.m; ++i) eval_perm[i] = t[i];
+    }
     if (src_pos)
       FMM_CUDA(cudaMemcpy(src_pos, T.src_pos.p, sizeof(double2) * T.n, cudaMemcpyDeviceToHost));
     if (src_g) FMM_CUDA(cudaMemcpy(src_g, T.src_g.p, sizeof(double) * T.n, cudaMemcpyDeviceToHost));
     if (eval_pos)
-      FMM_CUDA(cudaMemcpy(eval_pos, T.eval_pos.p, sizeof(double2) * T.m, cudaMemcpyDeviceToHost));
+      FMM_CUDA(cudaMemcpy(eval_pos, T.epos_t, sizeof(double2) * T.m, cudaMemcpyDeviceToHost));
     return FMM2D_OK;
   });
 }

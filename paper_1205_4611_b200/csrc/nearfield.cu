@@ -213,9 +213,8 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
   const long long nleaf = 1ll << (2 * T.L);
   note_launch();
   k_p2p<<<nblk(nleaf * 32, P2P_THREADS), P2P_THREADS, 0, st>>>(
-      T.L, offL, T.eval_leaf_off.as<int>(), Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(),
-      T.src_pos.as<double2>(), T.src_g.as<double>(), T.eval_pos.as<double2>(),
-      T.eval_perm.as<int>(), E.phi.as<double2>(), values, dstat);
+      T.L, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), T.src_pos.as<double2>(),
+      T.src_g.as<double>(), T.epos_t, T.eperm_t, E.phi.as<double2>(), values, dstat);
 }
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,

@@ -208,8 +208,8 @@ struct StepArgs {
 
 __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long long j, int s0,
                                                 int n, int2 x_first, int2 x_last, int2 y_first,
-                                                int2 y_last, int2 x_kth, int2 y_kth,
-                                                DevStatus* st, int* cut_rank_out,
+                                                int2 y_last, int2 x_kth, int2 y_kth, int2 x_next,
+                                                int2 y_next, DevStatus* st, int* cut_rank_out,
                                                 bool* along_y_out) {
   const Rect r = a.rect_tab[step_base(s) + j];
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
@@ -224,6 +224,13 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   }
   const int cr = along_y ? y_kth.y : x_kth.x;
   const double cut = along_y ? a.ys_sorted[cr] : a.xs_sorted[cr];  // tree.py:265
+  // evaluation points split by coord <= cut (tree.py:273): they follow the
+  // sources' median split exactly unless the (k+1)-th coordinate equals the cut
+  const int k = (n + 1) / 2;
+  if (k < n) {
+    const double nxt = along_y ? a.ys_sorted[y_next.y] : a.xs_sorted[x_next.x];
+    if (nxt == cut) atomicOr(&st->flags, ST_EVAL_TIES);
+  }
   a.cut_tab[step_base(s) + j] = cut;
   a.axis_tab[step_base(s) + j] = along_y;
   Rect lo = r, hi = r;                                              // tree.py:281-285
@@ -232,7 +239,7 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   a.rect_tab[step_base(s + 1) + 2 * j + 1] = hi;
   *cut_rank_out = cr;
   *along_y_out = along_y;
-  (void)n; (void)s0;
+  (void)s0;
 }
 
 __global__ void k_global_prepare(StepArgs a, int s, const int2* X0, const int2* X1,
@@ -249,8 +256,9 @@ __global__ void k_global_prepare(StepArgs a, int s, const int2* X0, const int2* 
   const int2* Y = yp ? Y1 : Y0;
   int cr;
   bool along_y;
+  const int kn = k < n ? k : k - 1;
   prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
-                  Y[s0 + k - 1], st, &cr, &along_y);
+                  Y[s0 + k - 1], X[s0 + kn], Y[s0 + kn], st, &cr, &along_y);
   cutrank[j] = cr;
   axis_cur[j] = along_y;
   // the copy ordered along the split axis stays put; the other one moves
@@ -446,8 +454,10 @@ k_subtree(SubArgs A, DevStatus* st) {
       const int s0 = off[j] - g0, nn = off[j + 1] - off[j], k = (nn + 1) / 2;
       int cr;
       bool along_y;
+      const int kn = k < nn ? k : k - 1;
       prepare_segment(A.a, s, j, s0, nn, sx[s0], sx[s0 + nn - 1], sy[s0], sy[s0 + nn - 1],
-                      sx[s0 + k - 1], sy[s0 + k - 1], st, &cr, &along_y);
+                      sx[s0 + k - 1], sy[s0 + k - 1], sx[s0 + kn], sy[s0 + kn], st, &cr,
+                      &along_y);
       q_s0[q] = s0;
       q_k[q] = k;
       q_cr[q] = cr;
@@ -851,8 +861,14 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                                                     T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                     T.src_perm.as<int>());
     }
-    // evaluation points: descend the cut table, stable sort by leaf
-    {
+    if (T.aliased && !T.eval_full) {
+      // evaluation points = sources, same partition (ties re-run the full path)
+      T.eleaf_t = nullptr;
+      T.epos_t = T.src_pos.as<double2>();
+      T.eperm_t = T.src_perm.as<int>();
+      T.eoff_t = P.d_off.as<int>() + off_base(S);
+    } else {
+      // evaluation points: descend the cut table, stable sort by leaf
       auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
       auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
       note_launch();
@@ -866,7 +882,10 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                                                     T.eval_perm.as<int>());
       note_launch();
       k_leaf_offsets<<<nblk(m + 1, 256), 256, 0, st>>>(kout, m, 1ll << S, T.eval_leaf_off.as<int>());
-      T.eval_leaf = kout;   // leaf id of every tree-ordered evaluation point
+      T.epos_t = T.eval_pos.as<double2>();
+      T.eperm_t = T.eval_perm.as<int>();
+      T.eoff_t = T.eval_leaf_off.as<int>();
+      T.eleaf_t = kout;
     }
   } else {
     // L == 0: a single box, identity permutations (tree.py:316-317)
@@ -876,15 +895,22 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n, pos, T.g_p,
                                                   T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                   T.src_perm.as<int>());
-    note_launch();
-    k_iota_perm<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m);
-    note_launch();
-    k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m, epos, nullptr,
-                                                  T.eval_pos.as<double2>(), nullptr,
-                                                  T.eval_perm.as<int>());
+    if (T.aliased) {
+      T.epos_t = T.src_pos.as<double2>();
+      T.eperm_t = T.src_perm.as<int>();
+    } else {
+      note_launch();
+      k_iota_perm<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m);
+      note_launch();
+      k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m, epos, nullptr,
+                                                    T.eval_pos.as<double2>(), nullptr,
+                                                    T.eval_perm.as<int>());
+      T.epos_t = T.eval_pos.as<double2>();
+      T.eperm_t = T.eval_perm.as<int>();
+    }
     note_launch();
     k_leaf_offsets_identity<<<1, 1, 0, st>>>(T.eval_leaf_off.as<int>(), m);
-    T.eval_leaf = nullptr;
+    T.eoff_t = T.eval_leaf_off.as<int>();
   }
   note_launch();
   k_level_geometry<<<nblk(nbox, 256), 256, 0, st>>>(L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
