@@ -128,6 +128,52 @@ int fmm2d_export_phi(fmm2d_ctx* ctx, double* phi_xy);
 int fmm2d_direct(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
                  int64_t m, const double* eval_xy, double* out_xy);
 
+/* ---------------------------------------------------------------------------
+ * Distributed evaluation (the reference is single-process,
+ * SPEC.md:409).  One context per rank, one rank per GPU.  The library runs the
+ * compute phases; the caller (paper_1205_4611_b200/distributed.py, through
+ * torch.distributed: NCCL over NVLink / NVSwitch) runs the collectives between
+ * them on `stream`.  All d_* arguments are device pointers; every phase
+ * function enqueues on `stream` and returns when host-visible results (counts)
+ * are ready.  Sequence per evaluation:
+ *   setup -> load -> [allreduce MIN bbox] -> root
+ *   for s < log2 G: (s even, s>0: segbox -> [allreduce MIN] -> check_segbox)
+ *                   8 x (hist -> [allreduce SUM] -> pick)
+ *                   eqcount -> [allgather] -> partition
+ *   send_counts -> [all-to-all records] -> build -> geom_pack -> [allgather]
+ *   -> connect -> 2 x request exchange [all-to-all ids, pack, all-to-all, unpack]
+ *      (particles before upward, multipoles after upward_top)
+ *   -> upward -> [allgather top multipoles] -> upward_top -> downward -> end
+ * --------------------------------------------------------------------------- */
+int fmm2d_dist_setup(fmm2d_ctx* ctx, int world_size, int rank, int64_t n_total, int p,
+                     double theta, int n_desired, void* stream, int32_t* n_levels);
+int fmm2d_dist_load(fmm2d_ctx* ctx, int64_t n_local, const double* d_pos_xy,
+                    const double* d_gamma, int64_t index_base, double* d_bbox4);
+int fmm2d_dist_root(fmm2d_ctx* ctx, const double* d_bbox4);
+int fmm2d_dist_segbox(fmm2d_ctx* ctx, int step, double* d_box);
+int fmm2d_dist_check_segbox(fmm2d_ctx* ctx, int step, const double* d_box);
+int fmm2d_dist_hist(fmm2d_ctx* ctx, int step, int round, int32_t* d_hist);
+int fmm2d_dist_pick(fmm2d_ctx* ctx, int step, int round, const int32_t* d_hist);
+int fmm2d_dist_eqcount(fmm2d_ctx* ctx, int step, int32_t* d_eq);
+int fmm2d_dist_partition(fmm2d_ctx* ctx, int step, const int32_t* d_eq_all);
+int fmm2d_dist_send_counts(fmm2d_ctx* ctx, int64_t* counts, void** d_records);
+int fmm2d_dist_build(fmm2d_ctx* ctx, const double* d_records, int64_t n_records,
+                     int64_t* owned_boxes);
+int fmm2d_dist_geom_pack(fmm2d_ctx* ctx, double* d_send);
+int fmm2d_dist_connect(fmm2d_ctx* ctx, const double* d_geometry_all, int64_t* request_counts);
+int fmm2d_dist_requests(fmm2d_ctx* ctx, int kind, const int32_t** d_ids);
+int fmm2d_dist_item_doubles(fmm2d_ctx* ctx, int kind, int64_t* n_doubles);
+int fmm2d_dist_pack(fmm2d_ctx* ctx, int kind, const int32_t* d_ids, int64_t n_ids,
+                    double* d_send);
+int fmm2d_dist_unpack(fmm2d_ctx* ctx, int kind, const double* d_recv);
+int fmm2d_dist_upward(fmm2d_ctx* ctx, double* d_top_send, int64_t* top_boxes);
+int fmm2d_dist_upward_top(fmm2d_ctx* ctx, const double* d_top_all);
+int fmm2d_dist_downward(fmm2d_ctx* ctx, double* d_values, int64_t* d_indices,
+                        fmm2d_report* rep);
+int fmm2d_scatter_values(fmm2d_ctx* ctx, int64_t n, const double* d_values,
+                         const int64_t* d_indices, double* d_out);
+int fmm2d_dist_end(fmm2d_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

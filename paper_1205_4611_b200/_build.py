@@ -18,7 +18,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libfmm2d.so"
 OBJ = PKG / "_obj"
-SOURCES = ["scan.cu", "tree.cu", "connect.cu", "expansions.cu", "nearfield.cu", "fmm2d.cu"]
+SOURCES = ["scan.cu", "tree.cu", "connect.cu", "expansions.cu", "nearfield.cu", "fmm2d.cu",
+           "dist.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-std=c++17", "-lineinfo",

@@ -68,6 +68,32 @@ _SIGS = {
     "fmm2d_export_expansions": (C.c_int, [C.c_void_p, _dp, _dp]),
     "fmm2d_export_phi": (C.c_int, [C.c_void_p, _dp]),
     "fmm2d_direct": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]),
+    # distributed evaluation (one rank; collectives issued by the caller)
+    "fmm2d_dist_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_double,
+                                   C.c_int, C.c_void_p, C.POINTER(C.c_int32)]),
+    "fmm2d_dist_load": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                  C.c_void_p]),
+    "fmm2d_dist_root": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fmm2d_dist_segbox": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "fmm2d_dist_check_segbox": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "fmm2d_dist_hist": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "fmm2d_dist_pick": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "fmm2d_dist_eqcount": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "fmm2d_dist_partition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "fmm2d_dist_send_counts": (C.c_int, [C.c_void_p, _i64p, C.POINTER(C.c_void_p)]),
+    "fmm2d_dist_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _i64p]),
+    "fmm2d_dist_geom_pack": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fmm2d_dist_connect": (C.c_int, [C.c_void_p, C.c_void_p, _i64p]),
+    "fmm2d_dist_requests": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "fmm2d_dist_item_doubles": (C.c_int, [C.c_void_p, C.c_int, _i64p]),
+    "fmm2d_dist_pack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
+    "fmm2d_dist_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "fmm2d_dist_upward": (C.c_int, [C.c_void_p, C.c_void_p, _i64p]),
+    "fmm2d_dist_upward_top": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fmm2d_dist_downward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Report)]),
+    "fmm2d_scatter_values": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]),
+    "fmm2d_dist_end": (C.c_int, [C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

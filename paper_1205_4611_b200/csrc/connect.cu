@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(CL_WARPS * 32)
 k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
            const int* __restrict__ ps_idx, int* so, int* sidx, long long scap, int* woff,
            int* widx, int* wtgt, long long wcap, LookbackState lbs, unsigned ntiles,
-           DevStatus* st) {
+           long long P0, long long P1, long long tb, long long te, DevStatus* st) {
   __shared__ unsigned s_mask[CL_WARPS][4][CL_MAXM];
   __shared__ int s_cnt[CL_WARPS][4][2];
   __shared__ long long s_excl[2];
@@ -52,16 +52,20 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned tile = s_tile;
-  const long long np = 1ll << (2 * (l - 1));
-  const long long P = (long long)tile * CL_WARPS + w;
+  // parents [P0, P1) of level l-1; their children outside the owned target
+  // window [tb, te) get empty lists (distributed ranks, Part)
+  const long long P = P0 + (long long)tile * CL_WARPS + w;
   const bool dead = lists_overflowed(st);
-  const bool live = P < np && !dead;
+  const bool live = P < P1 && !dead;
   const long long lb = level_base(l);
   int a0 = 0, ncand = 0;
   if (live) {
     a0 = ps_off[P];
     ncand = 4 * (ps_off[P + 1] - a0);
   }
+  bool own[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) own[j] = 4 * P + j >= tb && 4 * P + j < te;
   double rt[4], xt[4], yt[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -80,6 +84,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      if (!own[j]) continue;                                     // warp-uniform
       // d = |c_target - c_source| (geometry.py:40), then the θ-test (:41)
       const bool far = valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
       const unsigned m = __ballot_sync(0xffffffffu, far);
@@ -126,7 +131,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
     wb += nw[j];
     sb += ns[j];
   }
-  if (P < np && lane == 0) {
+  if (P < P1 && lane == 0) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       so[4 * P + j] = (int)spos[j];
@@ -140,8 +145,9 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
         wt += s_cnt[q][j][0];
         stt += s_cnt[q][j][1];
       }
-    so[4 * np] = (int)stt;
-    woff[lb + 4 * np] = (int)wt;
+    so[4 * P1] = (int)stt;
+    woff[lb + 4 * P1] = (int)wt;
+    woff[level_base(l + 1)] = (int)wt;     // next level's base (same slot when P1 = 4^(l-1))
   }
   if (!live) return;
   if (wb > wcap || sb > scap) {
@@ -156,7 +162,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
     const int c = c0 + lane;
     const bool valid = c < ncand;
     const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned vm0 = __ballot_sync(0xffffffffu, valid);
     double xc = 0.0, yc = 0.0, rc = 0.0;
     if ((c0 >> 5) >= CL_MAXM) {
       const long long gc = lb + cand;
@@ -166,6 +172,8 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      if (!own[j]) continue;
+      const unsigned vm = vm0;
       unsigned m;
       if ((c0 >> 5) < CL_MAXM) {
         m = s_mask[w][j][c0 >> 5];
@@ -195,7 +203,8 @@ __global__ void __launch_bounds__(CL_WARPS * 32)
 k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
              const int* __restrict__ s_idx, int* o_p2p, int* i_p2p, long long cap_p2p,
              int* o_p2l, int* i_p2l, long long cap_p2l, int* o_m2p, int* i_m2p,
-             long long cap_m2p, LookbackState lbs, unsigned ntiles, DevStatus* st) {
+             long long cap_m2p, LookbackState lbs, unsigned ntiles, long long tb, long long te,
+             DevStatus* st) {
   __shared__ unsigned s_mask[CL_WARPS][2][CL_MAXM];   // p2l, m2p masks (p2p = valid & ~both)
   __shared__ int s_cnt[CL_WARPS][3];
   __shared__ long long s_excl[3];
@@ -204,8 +213,8 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned tile = s_tile;
-  const long long nb = 1ll << (2 * L);
-  const long long b = (long long)tile * CL_WARPS + w;
+  const long long nb = te;                 // targets [tb, te) of the finest level
+  const long long b = tb + (long long)tile * CL_WARPS + w;
   const bool live = b < nb && !lists_overflowed(st);
   const long long lb = level_base(L);
   int a0 = 0, a1 = 0;
@@ -307,6 +316,14 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
   }
 }
 
+// off[i] for i outside the written window [lo, hi]: off[lo] before, off[hi] after
+__global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i < lo) off[i] = off[lo];
+  else if (i > hi) off[i] = off[hi];
+}
+
 __global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx) {
   weak_off[0] = 0;
   weak_off[1] = 0;     // the root has no far field (connectivity.py:106)
@@ -361,7 +378,7 @@ void compute_radius(TreeState& T, cudaStream_t st) {
 }
 
 void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus* dstat,
-                      cudaStream_t st) {
+                      cudaStream_t st, const Part& part) {
   const int L = T.L;
   const long long nbox = level_base(L + 1);
   const long long nleaf = 1ll << (2 * L);
@@ -408,42 +425,67 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   k_root_lists<<<1, 1, 0, st>>>(woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
-    const long long np = 1ll << (2 * (l - 1));
-    const unsigned ntiles = (unsigned)((np + CL_WARPS - 1) / CL_WARPS);
+    const long long tb = part.lo(l), te = part.hi(l);
+    const long long P0 = tb >> 2, P1 = (te + 3) >> 2;
+    const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS - 1) / CL_WARPS);
     note_launch();
     k_classify<<<ntiles, CL_WARPS * 32, 0, st>>>(
         l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
         Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
-        Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, dstat);
+        Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, P0, P1,
+        tb, te, dstat);
     cur = 1 - cur;
   }
   {
-    const unsigned ntiles = (unsigned)((nleaf + CL_WARPS - 1) / CL_WARPS);
+    const long long tb = part.lo(L), te = part.hi(L);
+    const unsigned ntiles = (unsigned)((te - tb + CL_WARPS - 1) / CL_WARPS);
     note_launch();
     k_reclassify<<<ntiles, CL_WARPS * 32, 0, st>>>(
         L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),
         Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
         Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles,
-        dstat);
+        tb, te, dstat);
+  }
+  if (part.G > 1) {
+    // empty lists for boxes this rank does not own: monotone CSR offsets
+    for (int l = 1; l <= L; ++l) {
+      note_launch();
+      k_csr_pad<<<nblk((1ll << (2 * l)) + 1, 256), 256, 0, st>>>(woff + level_base(l), 1ll << (2 * l),
+                                                           part.lo(l), part.hi(l));
+    }
+    for (DBuf* o : {&Ls.p2p_off, &Ls.p2l_off, &Ls.m2p_off}) {
+      note_launch();
+      k_csr_pad<<<nblk(nleaf + 1, 256), 256, 0, st>>>(o->as<int>(), nleaf, part.lo(L), part.hi(L));
+    }
   }
 }
 
-void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st) {
-  const long long nbox = level_base(T.L + 1);
-  const long long nleaf = 1ll << (2 * T.L);
+void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st,
+               const Part& part) {
+  const int L = T.L;
+  const long long nbox = level_base(L + 1);
+  const long long nleaf = 1ll << (2 * L);
   FMM_CUDA(cudaMemsetAsync(Ls.hist.p, 0, sizeof(int) * 4 * HIST_BINS, st));
-  note_launch();
-  k_histogram<<<std::min(nblk(nbox, 256), 296u), 256, 0, st>>>(Ls.weak_off.as<int>(), nbox, 0, Ls.hist.as<int>(),
-                                               dstat);
-  note_launch();
-  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.p2p_off.as<int>(), nleaf, 1,
-                                                Ls.hist.as<int>(), dstat);
-  note_launch();
-  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.p2l_off.as<int>(), nleaf, 2,
-                                                Ls.hist.as<int>(), dstat);
-  note_launch();
-  k_histogram<<<std::min(nblk(nleaf, 256), 296u), 256, 0, st>>>(Ls.m2p_off.as<int>(), nleaf, 3,
-                                                Ls.hist.as<int>(), dstat);
+  auto hist = [&](const int* off, long long n, int kind) {
+    if (n <= 0) return;
+    note_launch();
+    k_histogram<<<std::min(nblk(n, 256), 296u), 256, 0, st>>>(off, n, kind, Ls.hist.as<int>(),
+                                                              dstat);
+  };
+  if (part.G == 1) {
+    hist(Ls.weak_off.as<int>(), nbox, 0);
+  } else {
+    // owned boxes per level; shared (top) levels are counted by rank 0 only
+    for (int l = 0; l <= L; ++l) {
+      if (part.shared(l) && part.rank != 0) continue;
+      hist(Ls.weak_off.as<int>() + level_base(l) + part.lo(l), part.hi(l) - part.lo(l), 0);
+    }
+  }
+  const long long f0 = part.lo(L), f1 = part.hi(L);
+  hist(Ls.p2p_off.as<int>() + f0, f1 - f0, 1);
+  hist(Ls.p2l_off.as<int>() + f0, f1 - f0, 2);
+  hist(Ls.m2p_off.as<int>() + f0, f1 - f0, 3);
+  (void)nleaf;
 }
 
 }  // namespace fmm

@@ -3,6 +3,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -22,19 +23,27 @@ struct CudaError {
   CudaError(cudaError_t e, const char* call, const char* file, int line);
 };
 
-// grow-only device buffer
+// grow-only device buffer (owning; not copyable)
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
   void reserve(size_t nbytes);
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+  }
   template <class T> T* as() const { return static_cast<T*>(p); }
   ~DBuf();
 };
 
-// per (N, M, L) plan: data-independent segment offsets and partition tiles
+// per (N, M, L, s0) plan: data-independent segment offsets and partition tiles
+// (S = 2L - s0 split steps below the (sub)tree root)
 struct TreePlan {
   int64_t n = -1, m = -1;
-  int L = -1, S = 0, sb = 0;
+  int L = -1, s0 = -1, S = 0, sb = 0;
   int smem_bytes = 0;
   bool global_leaf_finalize = false;
   std::vector<int> tile_base;        // per global step s < sb: first tile index
@@ -47,8 +56,42 @@ __host__ __device__ inline int64_t step_base(int s) { return (int64_t(1) << s) -
 __host__ __device__ inline int64_t off_base(int s) { return (int64_t(1) << s) - 1 + s; }        // offset tables (+1 each)
 __host__ __device__ inline int64_t level_base(int l) { return ((int64_t(1) << (2 * l)) - 1) / 3; }  // boxes above level l
 
+// Ownership in a distributed evaluation: rank `rank` of
+// G = 2^s0 owns, at every level l with t = 2l - s0 >= 0, the contiguous boxes
+// [rank << t, (rank + 1) << t) -- the subtree below top-split segment
+// `rank`.  Levels above (2l < s0) are shared: every rank computes them
+// redundantly.  G = 1 owns everything.
+struct Part {
+  int G = 1, rank = 0, s0 = 0;
+  long long lo(int l) const {
+    const int t = 2 * l - s0;
+    return t < 0 ? 0 : (long long)rank << t;
+  }
+  long long hi(int l) const {
+    const int t = 2 * l - s0;
+    return t < 0 ? 1ll << (2 * l) : (long long)(rank + 1) << t;
+  }
+  bool shared(int l) const { return 2 * l < s0; }
+  int ltop() const { return (s0 + 1) / 2; }          // first level with owned boxes
+};
+
+// Which part of the global pyramid a tree build covers.  Single GPU: the
+// whole tree (s0 = 0).  Distributed: the subtree below segment `seg` of the
+// top split (s0 = log2 G steps, done collectively), written into global-size
+// output arrays at tree-order offset `out0`, with the original index of every
+// local input point in `orig`.
+struct TreeSpec {
+  int s0 = 0;
+  long long seg = 0;
+  long long out0 = 0;
+  const int* orig = nullptr;
+  bool root_given = false;
+  double root[4] = {0, 0, 0, 0};     // x0, x1, y0, y1
+};
+
 // device state of one tree (kept between phases of an evaluation)
 struct TreeState {
+  TreeSpec spec;
   int64_t n = 0, m = 0;
   int L = 0;
   bool aliased = true;
@@ -111,24 +154,31 @@ inline void note_launch() { ++g_launches; }
 // ---------------------------------------------------------------------------
 // launchers (all enqueue on `st`, no host sync)
 int plan_levels(int64_t n, int nd);
-void plan_tree(TreePlan& plan, int64_t n, int64_t m, int L);
+void plan_tree(TreePlan& plan, int64_t n, int64_t m, int L, int s0 = 0);
 void run_tree(TreeState& T, TreePlan& plan, DevStatus* dstat, cudaStream_t st);
 
 void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus* dstat,
-                      cudaStream_t st);
+                      cudaStream_t st, const Part& part = Part());
 
 void compute_radius(TreeState& T, cudaStream_t st);
 void run_upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                DevStatus* dstat, cudaStream_t st);
-void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st);
+                DevStatus* dstat, cudaStream_t st, const Part& part = Part());
+// M2M for parent levels lmax..lmin (descending); lmax < 0 means L-1
+void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part = Part(),
+             int lmin = 1, int lmax = -1);
 void run_m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
              cudaStream_t st);
-void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st);
+void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
+             const Part& part = Part());
+// L2P + M2P for tree-ordered evaluation points [e0, e1) (e1 < 0: all)
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
-                 cudaStream_t st);
+                 cudaStream_t st, long long e0 = 0, long long e1 = -1);
+// values in input order, or (out_base >= 0) tree order starting at point out_base
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-             double2* values, DevStatus* dstat, cudaStream_t st);
-void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st);
+             double2* values, DevStatus* dstat, cudaStream_t st, const Part& part = Part(),
+             long long out_base = -1);
+void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st,
+               const Part& part = Part());
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
                 double2* out, cudaStream_t st);

@@ -64,11 +64,11 @@ __device__ __forceinline__ cplx ld_coef(const double2* base, int j, int p) {
 // P2M (engine.py:67-82): one thread per leaf, sequential over its sources
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_p2m(int L, const int* __restrict__ offL, const double2* __restrict__ src_pos,
-      const double* __restrict__ src_g, const double* __restrict__ cx,
-      const double* __restrict__ cy, double2* mult, int p) {
-  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (b >= (1ll << (2 * L))) return;
+k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
+      const double2* __restrict__ src_pos, const double* __restrict__ src_g,
+      const double* __restrict__ cx, const double* __restrict__ cy, double2* mult, int p) {
+  const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= b1) return;
   const long long gb = level_base(L) + b;
   const double x0 = cx[gb], y0 = cy[gb];
   cplx acc[PM + 1];
@@ -95,13 +95,14 @@ k_p2m(int L, const int* __restrict__ offL, const double2* __restrict__ src_pos,
 // over the particles of its p2l source boxes (ascending), butterfly reduction
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_p2l(int L, const int* __restrict__ offL, const int* __restrict__ l_off,
-      const int* __restrict__ l_idx, const double2* __restrict__ src_pos,
-      const double* __restrict__ src_g, const double* __restrict__ cx,
-      const double* __restrict__ cy, double2* local, int p, DevStatus* st) {
-  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+k_p2l(int L, long long b0, long long b1, const int* __restrict__ offL,
+      const int* __restrict__ l_off, const int* __restrict__ l_idx,
+      const double2* __restrict__ src_pos, const double* __restrict__ src_g,
+      const double* __restrict__ cx, const double* __restrict__ cy, double2* local, int p,
+      DevStatus* st) {
+  const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
+  if (b >= b1 || lists_overflowed(st)) return;
   const long long lb = level_base(L);
   double2* out = local + (lb + b) * (p + 1);
   const int q0 = l_off[b], q1 = l_off[b + 1];
@@ -175,9 +176,10 @@ __device__ __forceinline__ void m2m_shift(cplx (&a)[PM + 1], cplx r) {
 
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_m2m(int l, const double* __restrict__ cx, const double* __restrict__ cy, double2* mult, int p) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= (1ll << (2 * l))) return;
+k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
+      const double* __restrict__ cy, double2* mult, int p) {
+  const long long k = k0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   const long long gp = level_base(l) + k;
   const long long gc0 = level_base(l + 1) + 4 * k;
   cplx acc[PM + 1];
@@ -203,11 +205,11 @@ k_m2m(int l, const double* __restrict__ cx, const double* __restrict__ cy, doubl
 // L2L (engine.py:126-129, operators.py:282-317): thread per child
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_l2l(int l, const double* __restrict__ cx, const double* __restrict__ cy, double2* local,
-      int p) {
-  // parent level l, child level l+1
-  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c >= (1ll << (2 * (l + 1)))) return;
+k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
+      const double* __restrict__ cy, double2* local, int p) {
+  // parent level l, child level l+1 (children [c0, c1))
+  const long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= c1) return;
   const long long gc = level_base(l + 1) + c;
   const long long gp = level_base(l) + (c >> 2);
   const double2* src = local + gp * (p + 1);
@@ -567,13 +569,14 @@ __global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __rest
 // share them), all loads of a row in flight at once.
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_l2p_m2p(long long m, int L, const unsigned* __restrict__ eleaf,
+k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __restrict__ eleaf,
           const double2* __restrict__ eval_pos, const int* __restrict__ m_off,
           const int* __restrict__ m_idx, const double* __restrict__ cx,
           const double* __restrict__ cy, const double2* __restrict__ mult,
           const double2* __restrict__ local, double2* phi, int p, DevStatus* st) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= m || lists_overflowed(st)) return;
+  // evaluation points [e0, e1) of m (tree order)
+  const long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= e1 || lists_overflowed(st)) return;
   const long long lb = level_base(L);
   const long long b = eleaf ? (long long)eleaf[e] : leaf_of_position(e, m, 2 * L);
   const double2 y = eval_pos[e];
@@ -610,26 +613,28 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 template <int PM>
 struct Launch {
   static void upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                     DevStatus* dstat, cudaStream_t st) {
+                     DevStatus* dstat, cudaStream_t st, const Part& part) {
     const int L = T.L, p = E.p;
     if (L == 0) return;
-    const long long nleaf = 1ll << (2 * L);
+    const long long b0 = part.lo(L), b1 = part.hi(L);
     note_launch();
-    k_p2m<PM><<<nblk(nleaf, 128), 128, 0, st>>>(L, offL, T.src_pos.as<double2>(),
-                                                T.src_g.as<double>(), T.box_cx.as<double>(),
-                                                T.box_cy.as<double>(), E.mult.as<double2>(), p);
+    k_p2m<PM><<<nblk(b1 - b0, 128), 128, 0, st>>>(L, b0, b1, offL, T.src_pos.as<double2>(),
+                                                  T.src_g.as<double>(), T.box_cx.as<double>(),
+                                                  T.box_cy.as<double>(), E.mult.as<double2>(), p);
     note_launch();
-    k_p2l<PM><<<nblk(nleaf * 32, 128), 128, 0, st>>>(
-        L, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
+    k_p2l<PM><<<nblk((b1 - b0) * 32, 128), 128, 0, st>>>(
+        L, b0, b1, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.local.as<double2>(), p, dstat);
   }
-  static void m2m(const TreeState& T, ExpState& E, cudaStream_t st) {
-    for (int l = T.L - 1; l >= 1; --l) {
+  static void m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part, int lmin,
+                  int lmax) {
+    for (int l = lmax; l >= lmin; --l) {
+      const long long k0 = part.lo(l), k1 = part.hi(l);
       note_launch();
-      k_m2m<PM><<<nblk(1ll << (2 * l), 128), 128, 0, st>>>(l, T.box_cx.as<double>(),
-                                                           T.box_cy.as<double>(),
-                                                           E.mult.as<double2>(), E.p);
+      k_m2m<PM><<<nblk(k1 - k0, 128), 128, 0, st>>>(l, k0, k1, T.box_cx.as<double>(),
+                                                    T.box_cy.as<double>(), E.mult.as<double2>(),
+                                                    E.p);
     }
   }
   static void m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
@@ -678,11 +683,13 @@ struct Launch {
                                            E.mult.as<double2>(), E.local.as<double2>(), E.p,
                                            dstat);
   }
-  static void l2l(const TreeState& T, ExpState& E, cudaStream_t st) {
+  static void l2l(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part) {
     for (int l = 1; l < T.L; ++l) {
+      const long long c0 = part.lo(l + 1), c1 = part.hi(l + 1);
       note_launch();
-      k_l2l<PM><<<nblk(1ll << (2 * (l + 1)), 128), 128, 0, st>>>(
-          l, T.box_cx.as<double>(), T.box_cy.as<double>(), E.local.as<double2>(), E.p);
+      k_l2l<PM><<<nblk(c1 - c0, 128), 128, 0, st>>>(l, c0, c1, T.box_cx.as<double>(),
+                                                    T.box_cy.as<double>(), E.local.as<double2>(),
+                                                    E.p);
     }
   }
 };
@@ -708,30 +715,37 @@ void dispatch_p(int p, F&& f) {
 bool p_supported(int p) { return p >= 1 && p <= 64; }
 
 void run_upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                DevStatus* dstat, cudaStream_t st) {
-  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::upward(T, Ls, E, offL, dstat, st); });
+                DevStatus* dstat, cudaStream_t st, const Part& part) {
+  dispatch_p(E.p, [&](auto pm) {
+    Launch<decltype(pm)::value>::upward(T, Ls, E, offL, dstat, st, part);
+  });
 }
-void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st) {
-  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::m2m(T, E, st); });
+void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part, int lmin,
+             int lmax) {
+  if (lmax < 0) lmax = T.L - 1;
+  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::m2m(T, E, st, part, lmin, lmax); });
 }
 void run_m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
              cudaStream_t st) {
   dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::m2l(T, Ls, E, dstat, st); });
 }
-void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st) {
+void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
+             const Part& part) {
   (void)dstat;
-  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::l2l(T, E, st); });
+  dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::l2l(T, E, st, part); });
 }
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
-                 cudaStream_t st) {
+                 cudaStream_t st, long long e0, long long e1) {
+  if (e1 < 0) e1 = T.m;
   if (T.L == 0) {   // a single box: no expansions (engine.py:257)
     FMM_CUDA(cudaMemsetAsync(E.phi.p, 0, sizeof(double2) * T.m, st));
     return;
   }
+  if (e1 <= e0) return;
   dispatch_p(E.p, [&](auto pm) {
     note_launch();
-    k_l2p_m2p<decltype(pm)::value><<<nblk(T.m, 128), 128, 0, st>>>(
-        T.m, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
+    k_l2p_m2p<decltype(pm)::value><<<nblk(e1 - e0, 128), 128, 0, st>>>(
+        T.m, e0, e1, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
         T.box_cx.as<double>(), T.box_cy.as<double>(), E.mult.as<double2>(),
         E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
   });

@@ -15,8 +15,7 @@
 #include <new>
 #include <string>
 
-#include "engine.h"
-#include "../../include/fmm2d.h"
+#include "context.h"
 
 namespace fmm {
 
@@ -50,66 +49,7 @@ DBuf::~DBuf() {
 
 }  // namespace fmm
 
-using namespace fmm;
-
-struct ApiError {
-  int code;
-  std::string msg;
-};
-
-struct fmm2d_ctx {
-  int device = 0;
-  cudaStream_t st = nullptr;
-  TreePlan plan;
-  TreeState T;
-  ListState Ls;
-  ExpState E;
-  DBuf d_status;
-  DevStatus* h_status = nullptr;
-  int* h_hist = nullptr;
-  cudaEvent_t ev[10] = {};
-  std::string err;
-  bool have_tree = false, have_lists = false, have_eval = false;
-  double theta = 0.5;
-  long long deg_info[4] = {0, 0, 0, 0};
-  double deg_xy[2] = {0, 0};
-};
-
-namespace {
-
-int fail(fmm2d_ctx* c, int code, const std::string& msg) {
-  if (c) c->err = msg;
-  return code;
-}
-
-template <class F>
-int guarded(fmm2d_ctx* c, F&& f) {
-  try {
-    c->err.clear();
-    return f();
-  } catch (const ApiError& e) {
-    return fail(c, e.code, e.msg);
-  } catch (const CudaError& e) {
-    if (e.err == cudaErrorMemoryAllocation) return fail(c, FMM2D_EOOM, e.what);
-    return fail(c, FMM2D_ECUDA, e.what);
-  } catch (const std::bad_alloc&) {
-    return fail(c, FMM2D_EOOM, "host allocation failed");
-  }
-}
-
-void reset_status(fmm2d_ctx* c) {
-  DevStatus init;
-  std::memset(&init, 0, sizeof init);
-  init.degenerate_key = ~0ull;
-  *c->h_status = init;
-  FMM_CUDA(cudaMemcpyAsync(c->d_status.p, c->h_status, sizeof(DevStatus),
-                           cudaMemcpyHostToDevice, c->st));
-}
-
-void fetch_status(fmm2d_ctx* c) {
-  FMM_CUDA(cudaMemcpyAsync(c->h_status, c->d_status.p, sizeof(DevStatus),
-                           cudaMemcpyDeviceToHost, c->st));
-}
+namespace fmm {
 
 void validate(int64_t n, int64_t m, int nd, double theta, int p, bool need_p) {
   if (n < 1) throw ApiError{FMM2D_EBADARG, "positions must be a non-empty 1-d complex array"};
@@ -188,15 +128,10 @@ void raise_degenerate(fmm2d_ctx* c) {
 void build_tree_impl(fmm2d_ctx* c, int nd) {
   TreeState& T = c->T;
   T.L = plan_levels(T.n, nd);
-  plan_tree(c->plan, T.n, T.m, T.L);
+  plan_tree(c->plan, T.n, T.m, T.L, 0);
   run_tree(T, c->plan, c->d_status.as<DevStatus>(), c->st);
 }
 
-float ev_ms(cudaEvent_t a, cudaEvent_t b) {
-  float ms = 0.f;
-  FMM_CUDA(cudaEventElapsedTime(&ms, a, b));
-  return ms;
-}
 
 int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, int64_t m,
                   const double* epos, int p, double theta, int nd, double* out,
@@ -338,6 +273,7 @@ int fmm2d_create(fmm2d_ctx** out, int device) {
   int rc = guarded(c, [&] {
     FMM_CUDA(cudaSetDevice(device));
     FMM_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_st = c->st;
     for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
     c->d_status.reserve(sizeof(DevStatus));
     FMM_CUDA(cudaMallocHost(&c->h_status, sizeof(DevStatus)));
@@ -360,9 +296,11 @@ void fmm2d_destroy(fmm2d_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->D.ev)
+    if (e) cudaEventDestroy(e);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_hist) cudaFreeHost(c->h_hist);
-  if (c->st) cudaStreamDestroy(c->st);
+  if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
 }
 

@@ -72,16 +72,16 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
 // 4-way unrolled, two accumulator pairs), then the G partial sums are folded
 // in fixed lane order -- deterministic, no atomics on values.
 __global__ void __launch_bounds__(P2P_THREADS)
-k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
+k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __restrict__ eoff,
       const int* __restrict__ n_off, const int* __restrict__ n_idx,
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double2* __restrict__ eval_pos, const int* __restrict__ eval_perm,
-      const double2* __restrict__ phi_in, double2* values, DevStatus* st) {
+      const double2* __restrict__ phi_in, double2* values, long long out_base, DevStatus* st) {
   __shared__ double2 s_pos[P2P_WARPS][P2P_CHUNK];
   __shared__ double s_g[P2P_WARPS][P2P_CHUNK];
-  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (b >= (1ll << (2 * L)) || lists_overflowed(st)) return;
+  if (b >= b1 || lists_overflowed(st)) return;
   const int e0 = eoff[b], e1 = eoff[b + 1];
   if (e0 == e1) return;
   const int q0 = n_off[b], q1 = n_off[b + 1];
@@ -163,7 +163,8 @@ k_p2p(int L, const int* __restrict__ soff, const int* __restrict__ eoff,
     if (active && grp == 0) {
       const int e = eb + ei;
       const double2 f = phi_in ? phi_in[e] : make_double2(0.0, 0.0);
-      values[eval_perm[e]] = make_double2(f.x + ax, f.y - ay);
+      // input order (engine.py:266-267), or tree order for distributed ranks
+      values[eval_perm ? (long long)eval_perm[e] : e - out_base] = make_double2(f.x + ax, f.y - ay);
     }
   }
   for (int d = 16; d; d >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, d);
@@ -209,12 +210,14 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-             double2* values, DevStatus* dstat, cudaStream_t st) {
-  const long long nleaf = 1ll << (2 * T.L);
+             double2* values, DevStatus* dstat, cudaStream_t st, const Part& part,
+             long long out_base) {
+  const long long b0 = part.lo(T.L), b1 = part.hi(T.L);
   note_launch();
-  k_p2p<<<nblk(nleaf * 32, P2P_THREADS), P2P_THREADS, 0, st>>>(
-      T.L, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), T.src_pos.as<double2>(),
-      T.src_g.as<double>(), T.epos_t, T.eperm_t, E.phi.as<double2>(), values, dstat);
+  k_p2p<<<nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0, st>>>(
+      b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), T.src_pos.as<double2>(),
+      T.src_g.as<double>(), T.epos_t, out_base >= 0 ? nullptr : T.eperm_t, E.phi.as<double2>(),
+      values, out_base, dstat);
 }
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,

@@ -204,6 +204,8 @@ struct StepArgs {
   const double* xs_sorted;
   const double* ys_sorted;
   int L;
+  int s0;                   // global step of local step 0 (subtree builds)
+  long long seg;            // global index of the local root segment at step s0
 };
 
 __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long long j, int s0,
@@ -213,11 +215,13 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
                                                 bool* along_y_out) {
   const Rect r = a.rect_tab[step_base(s) + j];
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
-  if ((s & 1) == 0 && (s >> 1) < a.L) {                             // tree.py:348
+  const int sg = s + a.s0;                                          // global step
+  if ((sg & 1) == 0 && (sg >> 1) < a.L) {                           // tree.py:348
     double xa = a.xs_sorted[x_first.x], xb = a.xs_sorted[x_last.x];
     double ya = a.ys_sorted[y_first.y], yb = a.ys_sorted[y_last.y];
     if (xa == xb && ya == yb) {
-      unsigned long long key = ((unsigned long long)(s >> 1) << 40) | (unsigned long long)j;
+      unsigned long long key = ((unsigned long long)(sg >> 1) << 40) |
+                               (unsigned long long)((a.seg << s) + j);
       atomicMin(&st->degenerate_key, key);
       atomicOr(&st->flags, ST_DEGENERATE);
     }
@@ -409,6 +413,8 @@ struct SubArgs {
   int* leaf_of;           // fallback: leaf id per original index
   bool in_smem_finalize;
   int nmax;
+  long long out0;         // tree-order offset of the outputs (subtree builds)
+  const int* orig;        // original index of every input point (null: identity)
 };
 
 __global__ void __launch_bounds__(SUB_THREADS)
@@ -529,8 +535,8 @@ k_subtree(SubArgs A, DevStatus* st) {
       const int me = sidx[i];
       int rank = 0;
       for (int t = l0; t < l1; ++t) rank += sidx[t] < me;
-      const int dst = g0 + l0 + rank;
-      A.src_perm[dst] = me;
+      const long long dst = A.out0 + g0 + l0 + rank;
+      A.src_perm[dst] = A.orig ? A.orig[me] : me;
       A.src_pos[dst] = A.pos[me];
       A.src_g[dst] = A.g[me];
     }
@@ -589,13 +595,14 @@ __global__ void k_iota_keys(const int* __restrict__ leaf_of, long long n, unsign
 
 __global__ void k_gather_points(const int* __restrict__ perm, long long m,
                                 const double2* __restrict__ pts, const double* __restrict__ g,
-                                double2* out_pos, double* out_g, int* out_perm) {
+                                double2* out_pos, double* out_g, int* out_perm,
+                                long long out0 = 0, const int* __restrict__ orig = nullptr) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= m) return;
   int e = perm[i];
-  out_perm[i] = e;
-  out_pos[i] = pts[e];
-  if (g) out_g[i] = g[e];
+  out_perm[out0 + i] = orig ? orig[e] : e;
+  out_pos[out0 + i] = pts[e];
+  if (g) out_g[out0 + i] = g[e];
 }
 
 // leaf offsets from leaf-sorted keys (handles empty leaves)
@@ -615,14 +622,17 @@ __global__ void k_leaf_offsets_identity(int* leaf_off, long long m) {
 
 // per-level box geometry from the rectangles of even steps (tree.py:375-377)
 __global__ void k_level_geometry(int L, const Rect* __restrict__ rect_tab, double* cx, double* cy,
-                                 double* hw, double* hh, double* r) {
+                                 double* hw, double* hh, double* r, int s0, long long seg) {
   long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = level_base(L + 1);
   if (gid >= total) return;
   int l = 0;
   while (level_base(l + 1) <= gid) ++l;
   const long long k = gid - level_base(l);
-  const Rect rc = rect_tab[step_base(2 * l) + k];
+  // subtree builds own boxes k in [seg << t, (seg + 1) << t) of level l, t = 2l - s0
+  const int t = 2 * l - s0;
+  if (t < 0 || (k >> t) != seg) return;
+  const Rect rc = rect_tab[step_base(t) + (k - (seg << t))];
   cx[gid] = (rc.x0 + rc.x1) / 2;
   cy[gid] = (rc.y0 + rc.y1) / 2;
   const double w = (rc.x1 - rc.x0) / 2, h = (rc.y1 - rc.y0) / 2;
@@ -658,9 +668,9 @@ int plan_levels(int64_t n, int nd) {
   return lev;
 }
 
-void plan_tree(TreePlan& P, int64_t n, int64_t m, int L) {
-  if (P.n == n && P.m == m && P.L == L) return;
-  P.n = n; P.m = m; P.L = L; P.S = 2 * L;
+void plan_tree(TreePlan& P, int64_t n, int64_t m, int L, int s0) {
+  if (P.n == n && P.m == m && P.L == L && P.s0 == s0) return;
+  P.n = n; P.m = m; P.L = L; P.s0 = s0; P.S = 2 * L - s0;
   const int S = P.S;
   // choose the first step whose segments fit one subtree CTA in SMEM
   auto nmax_at = [&](int s) { return (n + (int64_t(1) << s) - 1) >> s; };
@@ -727,14 +737,15 @@ void plan_tree(TreePlan& P, int64_t n, int64_t m, int L) {
 
 void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   const long long n = T.n, m = T.m;
-  const int L = T.L, S = 2 * L, sb = P.sb;
+  const TreeSpec& spec = T.spec;
+  const int L = T.L, S = 2 * L - spec.s0, sb = P.sb;
   const double2* pos = T.pos_p;
   const double2* epos = T.aliased ? pos : T.epos_p;
   const long long nseg_total = step_base(S + 1);
 
-  T.src_pos.reserve(sizeof(double2) * n);
-  T.src_g.reserve(sizeof(double) * n);
-  T.src_perm.reserve(sizeof(int) * n);
+  T.src_pos.reserve(sizeof(double2) * (spec.out0 + n));
+  T.src_g.reserve(sizeof(double) * (spec.out0 + n));
+  T.src_perm.reserve(sizeof(int) * (spec.out0 + n));
   T.eval_pos.reserve(sizeof(double2) * m);
   T.eval_perm.reserve(sizeof(int) * m);
   T.eval_leaf_off.reserve(sizeof(int) * ((1ll << S) + 1));
@@ -751,8 +762,12 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   T.vals_in.reserve(sizeof(int) * nmx);
   T.vals_out.reserve(sizeof(int) * nmx);
 
-  // root rectangle
-  {
+  // root rectangle: given (subtree of a distributed top split) or the tight bbox
+  if (spec.root_given) {
+    const Rect rr{spec.root[0], spec.root[1], spec.root[2], spec.root[3]};
+    FMM_CUDA(cudaMemcpyAsync(T.rect_tab.p, &rr, sizeof(Rect), cudaMemcpyHostToDevice, st));
+    FMM_CUDA(cudaStreamSynchronize(st));   // rr lives on this stack frame
+  } else {
     double* bb = T.bbox.as<double>();
     unsigned int* counter = reinterpret_cast<unsigned int*>(bb + 4 + 4 * 1024);
     FMM_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
@@ -802,7 +817,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                                                 T.ypar0.as<unsigned char>());
     StepArgs a{P.d_off.as<int>(), T.rect_tab.as<Rect>(), T.cut_tab.as<double>(),
                T.axis_tab.as<unsigned char>(), T.xs_sorted.as<double>(), T.ys_sorted.as<double>(),
-               L};
+               L, spec.s0, spec.seg};
     unsigned char *xp = T.xpar0.as<unsigned char>(), *yp = T.ypar0.as<unsigned char>();
     unsigned char *xq = T.xpar1.as<unsigned char>(), *yq = T.ypar1.as<unsigned char>();
     int* cutrank = T.cutrank.as<int>();
@@ -838,7 +853,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       SubArgs A{a, sb, S, X0, X1, Y0, Y1, xp, yp, T.perm_x.as<int>(), pos, T.g_p,
                 T.src_pos.as<double2>(), T.src_g.as<double>(), T.src_perm.as<int>(),
                 T.leaf_of.as<int>(), !P.global_leaf_finalize,
-                (int)((n + (1ll << sb) - 1) >> sb)};
+                (int)((n + (1ll << sb) - 1) >> sb), spec.out0, spec.orig};
       FMM_CUDA(cudaFuncSetAttribute(k_subtree, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     P.smem_bytes));
       note_launch();
@@ -859,7 +874,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       note_launch();
       k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_out.as<int>(), n, pos, T.g_p,
                                                     T.src_pos.as<double2>(), T.src_g.as<double>(),
-                                                    T.src_perm.as<int>());
+                                                    T.src_perm.as<int>(), spec.out0, spec.orig);
     }
     if (T.aliased && !T.eval_full) {
       // evaluation points = sources, same partition (ties re-run the full path)
@@ -894,7 +909,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     note_launch();
     k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n, pos, T.g_p,
                                                   T.src_pos.as<double2>(), T.src_g.as<double>(),
-                                                  T.src_perm.as<int>());
+                                                  T.src_perm.as<int>(), spec.out0, spec.orig);
     if (T.aliased) {
       T.epos_t = T.src_pos.as<double2>();
       T.eperm_t = T.src_perm.as<int>();
@@ -915,7 +930,8 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   note_launch();
   k_level_geometry<<<nblk(nbox, 256), 256, 0, st>>>(L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), T.box_hw.as<double>(),
-                                                    T.box_hh.as<double>(), T.box_r.as<double>());
+                                                    T.box_hh.as<double>(), T.box_r.as<double>(),
+                                                    spec.s0, spec.seg);
 }
 
 }  // namespace fmm

@@ -1,0 +1,68 @@
+"""Multi-rank path.
+
+CPU (no GPU needed): the collective layer of paper_1205_4611_b200.distributed
+with world_size 2 and 4 on the gloo backend.  GPU: the full distributed FMM
+with 2, 4 and 8 ranks sharing cuda:0 (gloo staging) against the single-GPU
+engine -- same tree, same lists, same values to roundoff."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+WORKER = ROOT / "tests" / "_dist_worker.py"
+
+
+def launch(nproc, mode, out, port, timeout=600):
+    env = dict(os.environ, PYTHONPATH=str(ROOT), OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(WORKER), mode, str(out)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_comm_layer_gloo(tmp_path, world):
+    out = tmp_path / "comm.json"
+    launch(world, "comm", out, 29561 + world)
+    parts = json.loads(out.read_text())
+    for r, res in enumerate(parts):
+        assert res["min"] == [1.0, -float(world - 1)]
+        assert res["sum"] == [world * (world + 1) // 2]
+        assert res["gather"] == [v for q in range(world) for v in (q, 10 * q)]
+        # rank r receives r+1 rows from every rank q, valued 100 q + r
+        assert res["recv_counts"] == [r + 1] * world
+        assert res["recv"] == [100.0 * q + r for q in range(world) for _ in range(r + 1)]
+        lo, hi = res["shard"]
+        assert (lo, hi) == ((1001 * r) // world, (1001 * (r + 1)) // world)
+        assert res["s0"] == {2: 1, 4: 2}[world]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,kind,n,p", [(2, "uniform", 20000, 17), (4, "normal", 30000, 20),
+                                            (8, "uniform", 40000, 20), (4, "layer", 25000, 12)])
+def test_distributed_matches_single_gpu(tmp_path, world, kind, n, p):
+    import paper_1205_4611_b200 as F
+    out = tmp_path / "dist.npz"
+    launch(world, f"engine:{kind}:{n}:{p}", out, 29600 + world + n % 97)
+    d = np.load(out)
+    pts = F.sample_points(F.DistributionSpec(kind, 0.01, 7), n)
+    cfg = F.TreeConfig(35, 0.5, p)
+    ref, rep = F.fmm_evaluate(pts, cfg, device=0)
+    vals = d["values"]
+    err = np.max(np.abs(vals - ref) / np.abs(ref))
+    assert err <= 1e-13, err
+    # rank 0's owned points: its subtree, values consistent with the gathered ones
+    np.testing.assert_array_equal(vals[d["idx"]], d["own"])
+    drep = json.loads(str(d["report"]))
+    assert drep["levels"] == rep.n_levels
+    assert drep["totals"] == rep.list_totals, (drep["totals"], rep.list_totals)
+    assert drep["skips"] == rep.coincident_skips
+    assert drep["hist"] == {k: {str(a): b for a, b in v.items()}
+                            for k, v in rep.list_histograms.items()}
