@@ -4,8 +4,10 @@
 Contract (one JSON line on rank 0):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config c1|c2|c3|c4|c5] [--n N]
-For N > 1 launch with torch.distributed.run; each rank evaluates its own
-independent problem of the configured size (replicas).
+For N > 1 launch with torch.distributed.run (one rank per GPU, NCCL): the
+distributed engine (paper_1205_4611_b200.distributed) evaluates
+one problem of N_gpus x N points, subtrees partitioned across the ranks
+(weak scaling).
 
 A "step" is one full fmm_evaluate (tree build through P2P and un-permute) of
 the configured point set.  `value` is measured with inputs resident in HBM
@@ -250,6 +252,118 @@ def run_ours(args, cfg, ws, rank, local):
     return out if rank == 0 else None
 
 
+def run_dist(args, cfg, ws, rank, local):
+    """N > 1 ranks (torchrun, one GPU each): the distributed engine on a weak-scaled
+    problem of ws x N points; device time = CUDA events on the
+    engine stream around one whole evaluation, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_1205_4611_b200 as F
+    from paper_1205_4611_b200 import _lib
+    from paper_1205_4611_b200.distributed import (Comm, engine_stream, evaluate_shard,
+                                                  fmm_evaluate_distributed, shard_bounds)
+
+    backend = os.environ.get("FMM2D_DIST_BACKEND", "nccl")
+    if backend != "nccl":              # test mode: several ranks may share one GPU
+        local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    comm = Comm()
+    if cfg["m"] is not None:
+        raise SystemExit("multi-GPU bench runs the aliased configurations (c2, c3, c5)")
+    tcfg = F.TreeConfig(35, 0.5, cfg["p"])
+    n_total = ws * cfg["n"]
+    pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 0), n_total)
+    lo, hi = shard_bounds(n_total, ws, rank)
+    st = engine_stream(local)
+    ctx = _lib.default_context(local)
+    with torch.cuda.stream(st):
+        d_pos = torch.from_numpy(pts.positions[lo:hi].view(np.float64).reshape(-1, 2)).to(dev)
+        d_g = torch.from_numpy(pts.strengths[lo:hi].copy()).to(dev)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        with torch.cuda.stream(st):
+            e0.record(st)
+            vals, idx, rep = evaluate_shard(ctx, comm, n_total, d_pos, d_g, lo, tcfg)
+            e1.record(st)
+        st.synchronize()
+        return e0.elapsed_time(e1), rep
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(local)
+    times, reps = [], []
+    barrier()
+    clocks.start()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ms, rep = step()
+        times.append(ms)
+        reps.append(rep)
+    barrier()
+    clk = clocks.stop()
+    ms_step = sum(times) / len(times)
+    phase = [sum(r.phase_ms[q] for r in reps) / len(reps) for q in range(8)]
+    # end to end: the public SPMD API with the full host point set on every rank
+    # (each rank uploads its shard, downloads the values it owns)
+    for _ in range(max(1, args.warmup // 2)):
+        fmm_evaluate_distributed(pts, tcfg, device=local, gather=False)
+    e2e = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        (own, idx), _ = fmm_evaluate_distributed(pts, tcfg, device=local, gather=False)
+        e2e.append(time.perf_counter() - t0)
+    barrier()
+    e2e_s = sum(e2e) / len(e2e)
+    t = torch.tensor([ms_step, e2e_s] + phase, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step, e2e_s, phase = float(t[0]), float(t[1]), [float(v) for v in t[2:]]
+    last = reps[-1]
+    pairs = int(last.list_totals[0])
+    m2l_ms = phase[4]
+    achieved = pairs * m2l_flops_per_pair(cfg["p"]) / (m2l_ms * 1e-3) / 1e12 if m2l_ms else 0.0
+    peak = json.loads(FP64_PEAK_FILE.read_text())["dfma_tflops"] if FP64_PEAK_FILE.exists() else 37.0
+    names = ["sort", "connect", "p2m", "m2m", "m2l", "l2l", "l2p", "p2p"]
+    out = {
+        "metric": METRIC, "value": n_total / (ms_step * 1e-3), "unit": "particles/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference sample_points generator, Philox seed 0), sharded by rank",
+        "config": {"workload": cfg["desc"] + f", weak-scaled to {ws} x N", "name": args.config,
+                   "n_sources": n_total, "n_per_gpu": cfg["n"], "p": cfg["p"], "theta": 0.5,
+                   "n_desired": 35, "distribution": cfg["kind"], "levels": int(last.n_levels),
+                   "parallelism": f"subtree domain decomposition x{ws} ({backend})",
+                   "l2": "flushed between timed steps (512 MiB write)"},
+        "phase_ms": {k: round(v, 4) for k, v in zip(names, phase)},
+        "e2e": {"value": n_total / e2e_s, "unit": "particles/s",
+                "h2d_bytes_per_step": 24 * (hi - lo), "d2h_bytes_per_step": 24 * len(own),
+                "ms_per_step": e2e_s * 1e3},
+        "roofline": {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic": f"rank-0 M2L pairs {pairs} x {m2l_flops_per_pair(cfg['p'])} "
+                                    "flop / slowest rank's M2L phase time"},
+        "clocks": clk,
+        "gpu_launches": int(last.kernel_launches) * args.steps,
+        "gpu_launches_per_step": int(last.kernel_launches),
+    }
+    dist.destroy_process_group()
+    return out if rank == 0 else None
+
+
 def cpu_baseline(cfg, n_sample):
     """Oracle port of the reference CPU path on a bounded sample of the same
     workload (same distribution and p, N = n_sample)."""
@@ -308,18 +422,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=None, help="override N (and M)")
+    ap.add_argument("--npoints", type=int, default=None, help="override N (and M)")
     ap.add_argument("--cpu-n", type=int, default=100_000, help="CPU baseline sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
-    if args.n:
-        cfg["n"] = args.n
+    if args.npoints:
+        cfg["n"] = args.npoints
         if cfg["m"] is not None:
-            cfg["m"] = args.n
+            cfg["m"] = args.npoints
     ws, rank, local = dist_env()
     if args.impl == "reference":
         out = run_reference(args, cfg, ws, rank)
+    elif ws > 1:
+        out = run_dist(args, cfg, ws, rank, local)
     else:
         out = run_ours(args, cfg, ws, rank, local)
     if out is not None:
