@@ -27,87 +27,91 @@ struct LevelGeo {
   const double* r;
 };
 
-constexpr int CL_WARPS = 8;     // warps (= parents, or finest targets) per CTA
-constexpr int CL_MAXM = 32;     // ballot masks cached per target (1024 candidates)
+constexpr int CL_WARPS = 8;     // warps per CTA
+constexpr int CL_PPW = 1;       // classify: parents (4 sibling targets each) per warp
+constexpr int CL_TPW = 8;       // reclassify: finest targets per warp
+constexpr int CL_MAXM = 16;     // ballot masks cached per target (512 candidates)
 
-// One level of classify_level (connectivity.py:47-68) in ONE pass: a warp per
-// parent box evaluates its four children against the children of the
-// parent's strong list (the siblings share that candidate set, so each
-// candidate's geometry is loaded once for four predicates); the far/near
-// ballot masks stay in SMEM; a decoupled look-back gives every target its
-// offsets in the global weak CSR and in the level's strong CSR; the lists
-// are then written compacted, ascending.  A CTA that finds the lists already
-// overflowed publishes zero counts (never stalls its successors) and writes
-// nothing; overflowing writes are skipped and flagged for the host's regrow.
+// One level of classify_level (connectivity.py:47-68) in ONE pass.  A warp
+// walks CL_PPW parent boxes; for each it evaluates the four children against
+// the children of the parent's strong list (the siblings share that candidate
+// set, so each candidate's geometry is loaded once for four predicates); the
+// far/near ballot masks stay in SMEM; one decoupled look-back per CTA
+// (CL_WARPS * CL_PPW parents) gives every target its offsets in the global
+// weak CSR and in the level's strong CSR; the lists are then written
+// compacted, ascending.  Children outside the owned window [tb, te) get empty
+// lists (distributed ranks).  A CTA that finds the lists already overflowed
+// publishes zero counts (never stalls its successors) and writes nothing.
 __global__ void __launch_bounds__(CL_WARPS * 32)
 k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
            const int* __restrict__ ps_idx, int* so, int* sidx, long long scap, int* woff,
            int* widx, int* wtgt, long long wcap, LookbackState lbs, unsigned ntiles,
            long long P0, long long P1, long long tb, long long te, DevStatus* st) {
-  __shared__ unsigned s_mask[CL_WARPS][4][CL_MAXM];
-  __shared__ int s_cnt[CL_WARPS][4][2];
+  __shared__ unsigned s_mask[CL_WARPS][CL_PPW][4][CL_MAXM];
+  __shared__ int s_cnt[CL_WARPS][CL_PPW][4][2];
   __shared__ long long s_excl[2];
   __shared__ unsigned s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned tile = s_tile;
-  // parents [P0, P1) of level l-1; their children outside the owned target
-  // window [tb, te) get empty lists (distributed ranks, Part)
-  const long long P = P0 + (long long)tile * CL_WARPS + w;
   const bool dead = lists_overflowed(st);
-  const bool live = P < P1 && !dead;
   const long long lb = level_base(l);
-  int a0 = 0, ncand = 0;
-  if (live) {
-    a0 = ps_off[P];
-    ncand = 4 * (ps_off[P + 1] - a0);
-  }
-  bool own[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) own[j] = 4 * P + j >= tb && 4 * P + j < te;
-  double rt[4], xt[4], yt[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const long long gb = lb + 4 * (live ? P : 0) + j;
-    rt[j] = geo.r[gb];
-    xt[j] = geo.cx[gb];
-    yt[j] = geo.cy[gb];
-  }
-  int nw[4] = {0, 0, 0, 0}, ns[4] = {0, 0, 0, 0};
-  for (int c0 = 0; c0 < ncand; c0 += 32) {
-    const int c = c0 + lane;
-    const bool valid = c < ncand;
-    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
-    const long long gc = lb + cand;
-    const double xc = geo.cx[gc], yc = geo.cy[gc], rc = geo.r[gc];
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!own[j]) continue;                                     // warp-uniform
-      // d = |c_target - c_source| (geometry.py:40), then the θ-test (:41)
-      const bool far = valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
-      const unsigned m = __ballot_sync(0xffffffffu, far);
-      if (lane == 0 && (c0 >> 5) < CL_MAXM) s_mask[w][j][c0 >> 5] = m;
-      nw[j] += __popc(m);
-      ns[j] += __popc(vm & ~m);
+  const long long Pw = P0 + ((long long)tile * CL_WARPS + w) * CL_PPW;   // this warp's first parent
+  auto cand_of = [&](int a0, int c) { return 4 * ps_idx[a0 + (c >> 2)] + (c & 3); };
+  // phase 1: predicates -> masks + counts
+  for (int u = 0; u < CL_PPW; ++u) {
+    const long long P = Pw + u;
+    const bool live = P < P1 && !dead;
+    int a0 = 0, ncand = 0;
+    if (live) {
+      a0 = ps_off[P];
+      ncand = 4 * (ps_off[P + 1] - a0);
     }
-  }
-  if (lane == 0) {
+    double rt[4], xt[4], yt[4];
+    bool own[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      s_cnt[w][j][0] = nw[j];
-      s_cnt[w][j][1] = ns[j];
+      own[j] = live && 4 * P + j >= tb && 4 * P + j < te;
+      const long long gb = lb + 4 * (live ? P : 0) + j;
+      rt[j] = geo.r[gb];
+      xt[j] = geo.cx[gb];
+      yt[j] = geo.cy[gb];
+    }
+    int nw[4] = {0, 0, 0, 0}, ns[4] = {0, 0, 0, 0};
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+      const int c = c0 + lane;
+      const bool valid = c < ncand;
+      const long long gc = lb + (valid ? cand_of(a0, c) : 0);
+      const double xc = geo.cx[gc], yc = geo.cy[gc], rc = geo.r[gc];
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!own[j]) continue;                                   // warp-uniform
+        // d = |c_target - c_source| (geometry.py:40), then the θ-test (:41)
+        const bool far =
+            valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
+        const unsigned m = __ballot_sync(0xffffffffu, far);
+        if (lane == 0 && (c0 >> 5) < CL_MAXM) s_mask[w][u][j][c0 >> 5] = m;
+        nw[j] += __popc(m);
+        ns[j] += __popc(vm & ~m);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s_cnt[w][u][j][0] = nw[j];
+        s_cnt[w][u][j][1] = ns[j];
+      }
     }
   }
   __syncthreads();
   if (w == 0) {
     long long agg[2] = {0, 0}, excl[2];
-    for (int q = 0; q < CL_WARPS; ++q)
-      for (int j = 0; j < 4; ++j) {
-        agg[0] += s_cnt[q][j][0];
-        agg[1] += s_cnt[q][j][1];
-      }
+    for (int q = 0; q < CL_WARPS * CL_PPW * 4; ++q) {
+      agg[0] += (&s_cnt[0][0][0][0])[2 * q];
+      agg[1] += (&s_cnt[0][0][0][0])[2 * q + 1];
+    }
     lb_prefix<2>(lbs, tile, agg, excl);
     if (lane == 0) {
       s_excl[0] = excl[0];
@@ -119,112 +123,116 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
   const long long wbase0 = woff[lb];
   long long wb = wbase0 + s_excl[0], sb = s_excl[1];
   for (int q = 0; q < w; ++q)
-    for (int j = 0; j < 4; ++j) {
-      wb += s_cnt[q][j][0];
-      sb += s_cnt[q][j][1];
-    }
-  long long wpos[4], spos[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    wpos[j] = wb;
-    spos[j] = sb;
-    wb += nw[j];
-    sb += ns[j];
-  }
-  if (P < P1 && lane == 0) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      so[4 * P + j] = (int)spos[j];
-      woff[lb + 4 * P + j] = (int)wpos[j];
-    }
-  }
-  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {   // totals: end of this level
-    long long wt = wbase0 + s_excl[0], stt = s_excl[1];
-    for (int q = 0; q < CL_WARPS; ++q)
+    for (int u = 0; u < CL_PPW; ++u)
       for (int j = 0; j < 4; ++j) {
-        wt += s_cnt[q][j][0];
-        stt += s_cnt[q][j][1];
+        wb += s_cnt[q][u][j][0];
+        sb += s_cnt[q][u][j][1];
+      }
+  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {   // totals: end of this level
+    long long wt = wb, stt = sb;
+    for (int u = 0; u < CL_PPW; ++u)
+      for (int j = 0; j < 4; ++j) {
+        wt += s_cnt[w][u][j][0];
+        stt += s_cnt[w][u][j][1];
       }
     so[4 * P1] = (int)stt;
     woff[lb + 4 * P1] = (int)wt;
     woff[level_base(l + 1)] = (int)wt;     // next level's base (same slot when P1 = 4^(l-1))
   }
-  if (!live) return;
-  if (wb > wcap || sb > scap) {
-    if (lane == 0) {
-      atomicOr(&st->flags, ST_OVERFLOW);
-      atomicOr(&st->overflow_where, 1);
-    }
-    return;
-  }
+  // phase 2: offsets and compacted lists
   const unsigned below = (1u << lane) - 1u;
-  for (int c0 = 0; c0 < ncand; c0 += 32) {
-    const int c = c0 + lane;
-    const bool valid = c < ncand;
-    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
-    const unsigned vm0 = __ballot_sync(0xffffffffu, valid);
-    double xc = 0.0, yc = 0.0, rc = 0.0;
-    if ((c0 >> 5) >= CL_MAXM) {
-      const long long gc = lb + cand;
-      xc = geo.cx[gc];
-      yc = geo.cy[gc];
-      rc = geo.r[gc];
-    }
+  for (int u = 0; u < CL_PPW; ++u) {
+    const long long P = Pw + u;
+    if (P >= P1) break;
+    long long wpos[4], spos[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (!own[j]) continue;
-      const unsigned vm = vm0;
-      unsigned m;
-      if ((c0 >> 5) < CL_MAXM) {
-        m = s_mask[w][j][c0 >> 5];
-      } else {
-        const bool far =
-            valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
-        m = __ballot_sync(0xffffffffu, far);
+      wpos[j] = wb;
+      spos[j] = sb;
+      wb += s_cnt[w][u][j][0];
+      sb += s_cnt[w][u][j][1];
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        so[4 * P + j] = (int)spos[j];
+        woff[lb + 4 * P + j] = (int)wpos[j];
       }
-      const unsigned sm = vm & ~m;
-      const long long gb = lb + 4 * P + j;
-      if ((m >> lane) & 1u) {
-        const long long o = wpos[j] + __popc(m & below);
-        widx[o] = (int)(lb + cand);
-        wtgt[o] = (int)gb;
+    }
+    if (dead) continue;
+    if (wb > wcap || sb > scap) {
+      if (lane == 0) {
+        atomicOr(&st->flags, ST_OVERFLOW);
+        atomicOr(&st->overflow_where, 1);
       }
-      if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
-      wpos[j] += __popc(m);
-      spos[j] += __popc(sm);
+      continue;
+    }
+    const int a0 = ps_off[P];
+    const int ncand = 4 * (ps_off[P + 1] - a0);
+    bool own[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) own[j] = 4 * P + j >= tb && 4 * P + j < te;
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+      const int c = c0 + lane;
+      const bool valid = c < ncand;
+      const int cand = valid ? cand_of(a0, c) : 0;
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      double xc = 0.0, yc = 0.0, rc = 0.0;
+      if ((c0 >> 5) >= CL_MAXM) {
+        const long long gc = lb + cand;
+        xc = geo.cx[gc];
+        yc = geo.cy[gc];
+        rc = geo.r[gc];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!own[j]) continue;
+        unsigned m;
+        if ((c0 >> 5) < CL_MAXM) {
+          m = s_mask[w][u][j][c0 >> 5];
+        } else {
+          const long long gb = lb + 4 * P + j;
+          const bool far = valid && well_separated(geo.r[gb], rc,
+                                                   numpy_cabs(geo.cx[gb] - xc, geo.cy[gb] - yc),
+                                                   theta);
+          m = __ballot_sync(0xffffffffu, far);
+        }
+        const unsigned sm = vm & ~m;
+        if ((m >> lane) & 1u) {
+          const long long o = wpos[j] + __popc(m & below);
+          widx[o] = (int)(lb + cand);
+          wtgt[o] = (int)(lb + 4 * P + j);
+        }
+        if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
+        wpos[j] += __popc(m);
+        spos[j] += __popc(sm);
+      }
     }
   }
 }
 
-// reclassify_finest (connectivity.py:71-96) in one pass: a warp per finest
-// target, kinds cached as ballot masks, three-counter look-back, compacted
-// ascending p2p / p2l / m2p lists.
+// reclassify_finest (connectivity.py:71-96) in one pass: a warp walks CL_TPW
+// finest targets, kinds cached as ballot masks, three-counter look-back per
+// CTA, compacted ascending p2p / p2l / m2p lists.
 __global__ void __launch_bounds__(CL_WARPS * 32)
 k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
              const int* __restrict__ s_idx, int* o_p2p, int* i_p2p, long long cap_p2p,
              int* o_p2l, int* i_p2l, long long cap_p2l, int* o_m2p, int* i_m2p,
              long long cap_m2p, LookbackState lbs, unsigned ntiles, long long tb, long long te,
              DevStatus* st) {
-  __shared__ unsigned s_mask[CL_WARPS][2][CL_MAXM];   // p2l, m2p masks (p2p = valid & ~both)
-  __shared__ int s_cnt[CL_WARPS][3];
+  __shared__ unsigned s_mask[CL_WARPS][CL_TPW][2][CL_MAXM];   // p2l, m2p (p2p = rest)
+  __shared__ int s_cnt[CL_WARPS][CL_TPW][3];
   __shared__ long long s_excl[3];
   __shared__ unsigned s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned tile = s_tile;
-  const long long nb = te;                 // targets [tb, te) of the finest level
-  const long long b = tb + (long long)tile * CL_WARPS + w;
-  const bool live = b < nb && !lists_overflowed(st);
+  const bool dead = lists_overflowed(st);
   const long long lb = level_base(L);
-  int a0 = 0, a1 = 0;
-  if (live) {
-    a0 = s_off[b];
-    a1 = s_off[b + 1];
-  }
-  const long long gt = lb + (live ? b : 0);
-  const double rt = geo.r[gt], xt = geo.cx[gt], yt = geo.cy[gt];
-  auto kinds = [&](int c, unsigned& ml, unsigned& mm, unsigned& vm, int& src) {
+  const long long bw = tb + ((long long)tile * CL_WARPS + w) * CL_TPW;
+  auto kinds = [&](long long b, double rt, double xt, double yt, int c, int a1, unsigned& ml,
+                   unsigned& mm, unsigned& vm, int& src) {
     const bool valid = c < a1;
     int kind = 0;   // 0 p2p, 1 p2l (larger source), 2 m2p (smaller source)
     src = valid ? s_idx[c] : 0;
@@ -239,30 +247,41 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
     ml = __ballot_sync(0xffffffffu, kind == 1);
     mm = __ballot_sync(0xffffffffu, kind == 2);
   };
-  int n0 = 0, n1 = 0, n2 = 0;
-  for (int c0 = a0; c0 < a1; c0 += 32) {
-    unsigned ml, mm, vm;
-    int src;
-    kinds(c0 + lane, ml, mm, vm, src);
-    const int ch = (c0 - a0) >> 5;
-    if (lane == 0 && ch < CL_MAXM) {
-      s_mask[w][0][ch] = ml;
-      s_mask[w][1][ch] = mm;
+  for (int u = 0; u < CL_TPW; ++u) {
+    const long long b = bw + u;
+    const bool live = b < te && !dead;
+    int a0 = 0, a1 = 0;
+    if (live) {
+      a0 = s_off[b];
+      a1 = s_off[b + 1];
     }
-    n0 += __popc(vm & ~(ml | mm));
-    n1 += __popc(ml);
-    n2 += __popc(mm);
-  }
-  if (lane == 0) {
-    s_cnt[w][0] = n0;
-    s_cnt[w][1] = n1;
-    s_cnt[w][2] = n2;
+    const long long gt = lb + (live ? b : 0);
+    const double rt = geo.r[gt], xt = geo.cx[gt], yt = geo.cy[gt];
+    int n0 = 0, n1 = 0, n2 = 0;
+    for (int c0 = a0; c0 < a1; c0 += 32) {
+      unsigned ml, mm, vm;
+      int src;
+      kinds(b, rt, xt, yt, c0 + lane, a1, ml, mm, vm, src);
+      const int ch = (c0 - a0) >> 5;
+      if (lane == 0 && ch < CL_MAXM) {
+        s_mask[w][u][0][ch] = ml;
+        s_mask[w][u][1][ch] = mm;
+      }
+      n0 += __popc(vm & ~(ml | mm));
+      n1 += __popc(ml);
+      n2 += __popc(mm);
+    }
+    if (lane == 0) {
+      s_cnt[w][u][0] = n0;
+      s_cnt[w][u][1] = n1;
+      s_cnt[w][u][2] = n2;
+    }
   }
   __syncthreads();
   if (w == 0) {
     long long agg[3] = {0, 0, 0}, excl[3];
-    for (int q = 0; q < CL_WARPS; ++q)
-      for (int k = 0; k < 3; ++k) agg[k] += s_cnt[q][k];
+    for (int q = 0; q < CL_WARPS * CL_TPW; ++q)
+      for (int k = 0; k < 3; ++k) agg[k] += (&s_cnt[0][0][0])[3 * q + k];
     lb_prefix<3>(lbs, tile, agg, excl);
     if (lane == 0)
       for (int k = 0; k < 3; ++k) s_excl[k] = excl[k];
@@ -270,49 +289,58 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
   __syncthreads();
   long long pos[3] = {s_excl[0], s_excl[1], s_excl[2]};
   for (int q = 0; q < w; ++q)
-    for (int k = 0; k < 3; ++k) pos[k] += s_cnt[q][k];
-  if (b < nb && lane == 0) {
-    o_p2p[b] = (int)pos[0];
-    o_p2l[b] = (int)pos[1];
-    o_m2p[b] = (int)pos[2];
-  }
+    for (int u = 0; u < CL_TPW; ++u)
+      for (int k = 0; k < 3; ++k) pos[k] += s_cnt[q][u][k];
   if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {
-    long long tot[3] = {s_excl[0], s_excl[1], s_excl[2]};
-    for (int q = 0; q < CL_WARPS; ++q)
-      for (int k = 0; k < 3; ++k) tot[k] += s_cnt[q][k];
-    o_p2p[nb] = (int)tot[0];
-    o_p2l[nb] = (int)tot[1];
-    o_m2p[nb] = (int)tot[2];
+    long long tot[3] = {pos[0], pos[1], pos[2]};
+    for (int u = 0; u < CL_TPW; ++u)
+      for (int k = 0; k < 3; ++k) tot[k] += s_cnt[w][u][k];
+    o_p2p[te] = (int)tot[0];
+    o_p2l[te] = (int)tot[1];
+    o_m2p[te] = (int)tot[2];
   }
-  if (!live) return;
-  if (pos[0] + n0 > cap_p2p || pos[1] + n1 > cap_p2l || pos[2] + n2 > cap_m2p) {
+  const unsigned below = (1u << lane) - 1u;
+  for (int u = 0; u < CL_TPW; ++u) {
+    const long long b = bw + u;
+    if (b >= te) break;
     if (lane == 0) {
+      o_p2p[b] = (int)pos[0];
+      o_p2l[b] = (int)pos[1];
+      o_m2p[b] = (int)pos[2];
+    }
+    const int n0 = s_cnt[w][u][0], n1 = s_cnt[w][u][1], n2 = s_cnt[w][u][2];
+    if (!dead && pos[0] + n0 <= cap_p2p && pos[1] + n1 <= cap_p2l && pos[2] + n2 <= cap_m2p) {
+      const int a0 = s_off[b], a1 = s_off[b + 1];
+      const long long gt = lb + b;
+      long long q0 = pos[0], q1 = pos[1], q2 = pos[2];
+      for (int c0 = a0; c0 < a1; c0 += 32) {
+        unsigned ml, mm, vm;
+        int src;
+        const int ch = (c0 - a0) >> 5;
+        if (ch < CL_MAXM) {
+          const int c = c0 + lane;
+          src = c < a1 ? s_idx[c] : 0;
+          vm = __ballot_sync(0xffffffffu, c < a1);
+          ml = s_mask[w][u][0][ch];
+          mm = s_mask[w][u][1][ch];
+        } else {
+          kinds(b, geo.r[gt], geo.cx[gt], geo.cy[gt], c0 + lane, a1, ml, mm, vm, src);
+        }
+        const unsigned mp = vm & ~(ml | mm);
+        if ((mp >> lane) & 1u) i_p2p[q0 + __popc(mp & below)] = src;
+        if ((ml >> lane) & 1u) i_p2l[q1 + __popc(ml & below)] = src;
+        if ((mm >> lane) & 1u) i_m2p[q2 + __popc(mm & below)] = src;
+        q0 += __popc(mp);
+        q1 += __popc(ml);
+        q2 += __popc(mm);
+      }
+    } else if (!dead && lane == 0) {
       atomicOr(&st->flags, ST_OVERFLOW);
       atomicOr(&st->overflow_where, 2);
     }
-    return;
-  }
-  const unsigned below = (1u << lane) - 1u;
-  for (int c0 = a0; c0 < a1; c0 += 32) {
-    unsigned ml, mm, vm;
-    int src;
-    const int ch = (c0 - a0) >> 5;
-    if (ch < CL_MAXM) {
-      const int c = c0 + lane;
-      src = c < a1 ? s_idx[c] : 0;
-      vm = __ballot_sync(0xffffffffu, c < a1);
-      ml = s_mask[w][0][ch];
-      mm = s_mask[w][1][ch];
-    } else {
-      kinds(c0 + lane, ml, mm, vm, src);
-    }
-    const unsigned mp = vm & ~(ml | mm);
-    if ((mp >> lane) & 1u) i_p2p[pos[0] + __popc(mp & below)] = src;
-    if ((ml >> lane) & 1u) i_p2l[pos[1] + __popc(ml & below)] = src;
-    if ((mm >> lane) & 1u) i_m2p[pos[2] + __popc(mm & below)] = src;
-    pos[0] += __popc(mp);
-    pos[1] += __popc(ml);
-    pos[2] += __popc(mm);
+    pos[0] += n0;
+    pos[1] += n1;
+    pos[2] += n2;
   }
 }
 
@@ -402,7 +430,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   Ls.hist.reserve(sizeof(int) * 4 * HIST_BINS);
 
   // look-back state: flags + 3 counters per tile, grow-only, epoch-tagged
-  const long long max_tiles = (nleaf + CL_WARPS - 1) / CL_WARPS + 1;
+  const long long max_tiles = (nleaf + CL_WARPS - 1) / CL_WARPS + 1;   // >= tiles of any launch
   if (Ls.lb_tiles < max_tiles) {
     Ls.lb_flags.reserve(sizeof(unsigned) * max_tiles);
     Ls.lb_vals.reserve(sizeof(long long) * 6 * max_tiles);
@@ -427,7 +455,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   for (int l = 1; l <= L; ++l) {
     const long long tb = part.lo(l), te = part.hi(l);
     const long long P0 = tb >> 2, P1 = (te + 3) >> 2;
-    const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS - 1) / CL_WARPS);
+    const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
     note_launch();
     k_classify<<<ntiles, CL_WARPS * 32, 0, st>>>(
         l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
@@ -438,7 +466,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   }
   {
     const long long tb = part.lo(L), te = part.hi(L);
-    const unsigned ntiles = (unsigned)((te - tb + CL_WARPS - 1) / CL_WARPS);
+    const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
     note_launch();
     k_reclassify<<<ntiles, CL_WARPS * 32, 0, st>>>(
         L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),

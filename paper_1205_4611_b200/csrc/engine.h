@@ -105,6 +105,9 @@ struct TreeState {
   DBuf X0, X1, Y0, Y1;               // int2 (rank_x, rank_y) arrays
   DBuf xpar0, xpar1, ypar0, ypar1, cutrank;
   DBuf tile_cnt, tile_pre;
+  DBuf lb_flags, lb_vals, lb_ticket;  // look-back state of the fused partition steps
+  long long lb_tiles = 0;
+  unsigned lb_epoch = 0;
   DBuf rect_tab, cut_tab, axis_tab;
   DBuf leaf_of;                      // eval/source leaf ids (fallback + evals)
   // outputs (tree order)

@@ -91,8 +91,11 @@ k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
     if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
 }
 
-// P2L (engine.py:85-93, operators.py:209-224): one warp per target leaf, lanes
-// over the particles of its p2l source boxes (ascending), butterfly reduction
+// P2L (engine.py:85-93, operators.py:209-224): one thread per target leaf;
+// b_k += sum_i g_i w_i^(k+1), w_i = 1/(z_i - z0), over the particles of its
+// p2l source leaves in ascending order.  P2L lists are short (~1 source leaf
+// per target), so a thread's sequential power chain is cheaper than any
+// cross-lane reduction of the (p+1)-term rows.
 template <int PM>
 __global__ void __launch_bounds__(128)
 k_p2l(int L, long long b0, long long b1, const int* __restrict__ offL,
@@ -100,47 +103,38 @@ k_p2l(int L, long long b0, long long b1, const int* __restrict__ offL,
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double* __restrict__ cx, const double* __restrict__ cy, double2* local, int p,
       DevStatus* st) {
-  const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
+  const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (b >= b1 || lists_overflowed(st)) return;
   const long long lb = level_base(L);
   double2* out = local + (lb + b) * (p + 1);
   const int q0 = l_off[b], q1 = l_off[b + 1];
-  if (q0 == q1) {                    // no p2l sources: local starts at zero
-    for (int j = lane; j <= p; j += 32) out[j] = make_double2(0.0, 0.0);
-    return;
-  }
-  const double x0 = cx[lb + b], y0 = cy[lb + b];
   cplx acc[PM + 1];
 #pragma unroll
   for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
-  for (int q = q0; q < q1; ++q) {
-    const int a = l_idx[q];
-    for (int i = offL[a] + lane; i < offL[a + 1]; i += 32) {
-      const double2 z = src_pos[i];
-      const cplx d{z.x - x0, z.y - y0};
-      if (d.x == 0.0 && d.y == 0.0) {
-        atomicOr(&st->flags, ST_P2L_SINGULAR);
-        continue;
-      }
-      const cplx inv = crcp_fast(d);
-      cplx w = cscale(inv, src_g[i]);
+  if (q0 < q1) {
+    const double x0 = cx[lb + b], y0 = cy[lb + b];
+    for (int q = q0; q < q1; ++q) {
+      const int a = l_idx[q];
+      for (int i = offL[a]; i < offL[a + 1]; ++i) {
+        const double2 z = src_pos[i];
+        const cplx d{z.x - x0, z.y - y0};
+        if (d.x == 0.0 && d.y == 0.0) {
+          atomicOr(&st->flags, ST_P2L_SINGULAR);
+          continue;
+        }
+        const cplx inv = crcp_fast(d);
+        cplx w = cscale(inv, src_g[i]);
 #pragma unroll
-      for (int k = 0; k <= PM; ++k) {
-        acc[k] = cadd(acc[k], w);
-        w = cmul(w, inv);
+        for (int k = 0; k <= PM; ++k) {
+          acc[k] = cadd(acc[k], w);
+          w = cmul(w, inv);
+        }
       }
     }
   }
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) {
-#pragma unroll
-    for (int d = 16; d; d >>= 1) {
-      acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, d);
-      acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, d);
-    }
-    if (j <= p && (j & 31) == lane) out[j] = make_double2(acc[j].x, acc[j].y);
-  }
+  for (int j = 0; j <= PM; ++j)
+    if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
 }
 
 // --------------------------------------------------------------------------
@@ -174,31 +168,34 @@ __device__ __forceinline__ void m2m_shift(cplx (&a)[PM + 1], cplx r) {
   }
 }
 
+// four threads per parent (one per child shift), children summed in order
+// 0..3 through shuffles (engine.py:100 reshape(-1, 4, p+1).sum(1))
 template <int PM>
 __global__ void __launch_bounds__(128)
 k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* mult, int p) {
-  const long long k = k0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= k1) return;
-  const long long gp = level_base(l) + k;
-  const long long gc0 = level_base(l + 1) + 4 * k;
-  cplx acc[PM + 1];
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long k = k0 + (t >> 2);
+  const int c = (int)(t & 3), lane = threadIdx.x & 31;
+  const bool valid = k < k1;
+  const long long kk = valid ? k : k0;
+  const long long gp = level_base(l) + kk;
+  const long long gc = level_base(l + 1) + 4 * kk + c;
+  const double2* src = mult + gc * (p + 1);
+  cplx a[PM + 1];
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
-  for (int c = 0; c < 4; ++c) {
-    const long long gc = gc0 + c;
-    const double2* src = mult + gc * (p + 1);
-    cplx a[PM + 1];
-#pragma unroll
-    for (int j = 0; j <= PM; ++j) a[j] = ld_coef(src, j, p);
-    m2m_shift<PM>(a, cplx{cx[gc] - cx[gp], cy[gc] - cy[gp]});   // child - parent
-#pragma unroll
-    for (int j = 0; j <= PM; ++j) acc[j] = cadd(acc[j], a[j]);
-  }
+  for (int j = 0; j <= PM; ++j) a[j] = ld_coef(src, j, p);
+  m2m_shift<PM>(a, cplx{cx[gc] - cx[gp], cy[gc] - cy[gp]});   // child - parent
+  const int g0 = lane & ~3;
   double2* out = mult + gp * (p + 1);
 #pragma unroll
-  for (int j = 0; j <= PM; ++j)
-    if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
+  for (int j = 0; j <= PM; ++j) {
+    const double x0 = __shfl_sync(0xffffffffu, a[j].x, g0), y0 = __shfl_sync(0xffffffffu, a[j].y, g0);
+    const double x1 = __shfl_sync(0xffffffffu, a[j].x, g0 + 1), y1 = __shfl_sync(0xffffffffu, a[j].y, g0 + 1);
+    const double x2 = __shfl_sync(0xffffffffu, a[j].x, g0 + 2), y2 = __shfl_sync(0xffffffffu, a[j].y, g0 + 2);
+    const double x3 = __shfl_sync(0xffffffffu, a[j].x, g0 + 3), y3 = __shfl_sync(0xffffffffu, a[j].y, g0 + 3);
+    if (valid && c == 0 && j <= p) out[j] = make_double2(((x0 + x1) + x2) + x3, ((y0 + y1) + y2) + y3);
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -622,7 +619,7 @@ struct Launch {
                                                   T.src_g.as<double>(), T.box_cx.as<double>(),
                                                   T.box_cy.as<double>(), E.mult.as<double2>(), p);
     note_launch();
-    k_p2l<PM><<<nblk((b1 - b0) * 32, 128), 128, 0, st>>>(
+    k_p2l<PM><<<nblk(b1 - b0, 128), 128, 0, st>>>(
         L, b0, b1, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.local.as<double2>(), p, dstat);
@@ -632,7 +629,7 @@ struct Launch {
     for (int l = lmax; l >= lmin; --l) {
       const long long k0 = part.lo(l), k1 = part.hi(l);
       note_launch();
-      k_m2m<PM><<<nblk(k1 - k0, 128), 128, 0, st>>>(l, k0, k1, T.box_cx.as<double>(),
+      k_m2m<PM><<<nblk(4 * (k1 - k0), 128), 128, 0, st>>>(l, k0, k1, T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), E.mult.as<double2>(),
                                                     E.p);
     }

@@ -30,19 +30,21 @@ __device__ __forceinline__ unsigned lb_ticket(const LookbackState& S, unsigned n
 // by one full warp (all 32 lanes, same arguments).  The warp inspects a
 // window of 32 predecessors per step (CUB-style), so a wave of tiles that
 // publish together resolves in a few L2 round trips instead of one per tile.
+// `head` starts a new chain (segmented scans: the first tile of a segment)
 template <int NW>
 __device__ __forceinline__ void lb_prefix(const LookbackState& S, unsigned tile,
-                                          const long long (&agg)[NW], long long (&excl)[NW]) {
+                                          const long long (&agg)[NW], long long (&excl)[NW],
+                                          bool head = false) {
   const unsigned tag = S.epoch << 2;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int w = 0; w < NW; ++w) excl[w] = 0;
-  if (tile == 0) {
+  if (tile == 0 || head) {
     if (lane == 0) {
 #pragma unroll
-      for (int w = 0; w < NW; ++w) S.incv[w] = agg[w];
+      for (int w = 0; w < NW; ++w) S.incv[(long long)tile * NW + w] = agg[w];
       __threadfence();
-      atomicExch(S.flag, tag | 2u);
+      atomicExch(S.flag + tile, tag | 2u);
     }
     __syncwarp();
     return;

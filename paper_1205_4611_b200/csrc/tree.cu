@@ -21,6 +21,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "engine.h"
+#include "lookback.cuh"
 
 namespace fmm {
 
@@ -246,118 +247,53 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   (void)s0;
 }
 
-__global__ void k_global_prepare(StepArgs a, int s, const int2* X0, const int2* X1,
-                                 const int2* Y0, const int2* Y1, const unsigned char* xpar,
-                                 const unsigned char* ypar, unsigned char* xpar_next,
-                                 unsigned char* ypar_next, int* cutrank, unsigned char* axis_cur,
-                                 DevStatus* st) {
-  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= (1ll << s)) return;
-  const int* off = a.off + off_base(s);
-  const int s0 = off[j], n = off[j + 1] - s0, k = (n + 1) / 2;
-  const unsigned char xp = xpar[j], yp = ypar[j];
-  const int2* X = xp ? X1 : X0;
-  const int2* Y = yp ? Y1 : Y0;
-  int cr;
-  bool along_y;
-  const int kn = k < n ? k : k - 1;
-  prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
-                  Y[s0 + k - 1], X[s0 + kn], Y[s0 + kn], st, &cr, &along_y);
-  cutrank[j] = cr;
-  axis_cur[j] = along_y;
-  // the copy ordered along the split axis stays put; the other one moves
-  const unsigned char nxp = along_y ? (unsigned char)(1 - xp) : xp;
-  const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
-  xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
-  ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
-}
-
 // stable partition of the moving copy, tiles aligned to segments
 __device__ __forceinline__ bool part_flag(int2 e, bool along_y, int cr) {
   return (along_y ? e.y : e.x) <= cr;
 }
 
+// One global split step in ONE pass (replaces prepare / count / scan /
+// scatter): tiles are segment-aligned and taken in ticket order; every tile
+// derives its segment's axis and cut rank, the segment's first tile also
+// writes the step tables (cut, axis, child rectangles, parities, checks); a
+// segmented decoupled look-back gives each tile the number of left-going
+// elements of its segment before it; the stable partition is then written.
 __global__ void __launch_bounds__(PART_THREADS)
-k_part_count(int s, const int* __restrict__ tile_seg, const int* __restrict__ tile_start,
-             const int* __restrict__ off_all, const int2* X0, const int2* X1, const int2* Y0,
-             const int2* Y1, const unsigned char* xpar, const unsigned char* ypar,
-             const int* __restrict__ cutrank, const unsigned char* __restrict__ axis_cur,
-             int* tile_cnt) {
-  const int t = blockIdx.x;
-  const int j = tile_seg[t];
-  const int* off = off_all + off_base(s);
-  const int end = off[j + 1];
-  const bool along_y = axis_cur[j];
-  const int2* M = along_y ? (xpar[j] ? X1 : X0) : (ypar[j] ? Y1 : Y0);
-  const int cr = cutrank[j];
-  const int base = tile_start[t] + threadIdx.x * PART_ITEMS;
-  int c = 0;
-#pragma unroll
-  for (int q = 0; q < PART_ITEMS; ++q) {
-    int i = base + q;
-    if (i < end && i < tile_start[t] + PART_TILE) c += part_flag(M[i], along_y, cr);
-  }
-  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
+            const int* __restrict__ tile_start, int2* X0, int2* X1, int2* Y0, int2* Y1,
+            const unsigned char* xpar, const unsigned char* ypar, unsigned char* xpar_next,
+            unsigned char* ypar_next, LookbackState lbs, unsigned ntiles, DevStatus* st) {
+  __shared__ unsigned s_tile;
   __shared__ int sw[PART_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = c;
+  __shared__ long long s_excl;
+  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int q = 0; q < PART_THREADS / 32; ++q) tot += sw[q];
-    tile_cnt[t] = tot;
-  }
-}
-
-// segmented exclusive scan of tile counts (tiles of one segment are contiguous)
-__global__ void k_part_scan(int ntiles, const int* __restrict__ tile_seg,
-                            const int* __restrict__ tile_cnt, int* tile_pre) {
-  __shared__ int s_carry_seg, s_carry;
-  __shared__ int s_val[1024], s_seg[1024];
-  if (threadIdx.x == 0) { s_carry_seg = -1; s_carry = 0; }
-  __syncthreads();
-  for (int b = 0; b < ntiles; b += blockDim.x) {
-    int t = b + threadIdx.x;
-    int v = t < ntiles ? tile_cnt[t] : 0;
-    int sg = t < ntiles ? tile_seg[t] : 0x7fffffff;
-    s_val[threadIdx.x] = v;
-    s_seg[threadIdx.x] = sg;
-    __syncthreads();
-    // inclusive segmented Hillis-Steele in smem
-    for (int d = 1; d < (int)blockDim.x; d <<= 1) {
-      int add = 0;
-      if ((int)threadIdx.x >= d && s_seg[threadIdx.x - d] == sg) add = s_val[threadIdx.x - d];
-      __syncthreads();
-      s_val[threadIdx.x] += add;
-      __syncthreads();
-    }
-    int incl = s_val[threadIdx.x];
-    int carry = (sg == s_carry_seg) ? s_carry : 0;
-    if (t < ntiles) tile_pre[t] = carry + incl - v;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) {
-      s_carry = carry + incl;
-      s_carry_seg = sg;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(PART_THREADS)
-k_part_scatter(int s, const int* __restrict__ tile_seg, const int* __restrict__ tile_start,
-               const int* __restrict__ off_all, int2* X0, int2* X1, int2* Y0, int2* Y1,
-               const unsigned char* xpar, const unsigned char* ypar,
-               const int* __restrict__ cutrank, const unsigned char* __restrict__ axis_cur,
-               const int* __restrict__ tile_pre) {
-  const int t = blockIdx.x;
+  const unsigned t = s_tile;
   const int j = tile_seg[t];
-  const int* off = off_all + off_base(s);
-  const int s0 = off[j], end = off[j + 1], k = (end - s0 + 1) / 2;
-  const bool along_y = axis_cur[j];
-  const bool mp = along_y ? xpar[j] : ypar[j];
-  const int2* M = along_y ? (mp ? X1 : X0) : (mp ? Y1 : Y0);
-  int2* D = along_y ? (mp ? X0 : X1) : (mp ? Y0 : Y1);
-  const int cr = cutrank[j];
+  const int* off = a.off + off_base(s);
+  const int s0 = off[j], end = off[j + 1], n = end - s0, k = (n + 1) / 2;
+  const unsigned char xp = xpar[j], yp = ypar[j];
+  const int2* X = xp ? X1 : X0;
+  const int2* Y = yp ? Y1 : Y0;
   const int tstart = tile_start[t];
+  const bool head = tstart == s0;
+  const Rect r = a.rect_tab[step_base(s) + j];
+  const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
+  const int cr = along_y ? Y[s0 + k - 1].y : X[s0 + k - 1].x;
+  if (head && threadIdx.x == 0) {
+    int cr2;
+    bool ay2;
+    const int kn = k < n ? k : k - 1;
+    prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
+                    Y[s0 + k - 1], X[s0 + kn], Y[s0 + kn], st, &cr2, &ay2);
+    // the copy ordered along the split axis stays put; the other one moves
+    const unsigned char nxp = along_y ? (unsigned char)(1 - xp) : xp;
+    const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
+    xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
+    ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
+  }
+  const int2* M = along_y ? X : Y;
+  int2* D = along_y ? (xp ? X0 : X1) : (yp ? Y0 : Y1);
   const int tend = min(end, tstart + PART_TILE);
   const int base = tstart + threadIdx.x * PART_ITEMS;
   int2 e[PART_ITEMS];
@@ -365,7 +301,7 @@ k_part_scatter(int s, const int* __restrict__ tile_seg, const int* __restrict__ 
   int c = 0;
 #pragma unroll
   for (int q = 0; q < PART_ITEMS; ++q) {
-    int i = base + q;
+    const int i = base + q;
     f[q] = false;
     if (i < tend) {
       e[q] = M[i];
@@ -373,24 +309,30 @@ k_part_scatter(int s, const int* __restrict__ tile_seg, const int* __restrict__ 
       c += f[q];
     }
   }
-  // block exclusive scan of c
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int incl = c;
+#pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    int o = __shfl_up_sync(0xffffffffu, incl, d);
+    const int o = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += o;
   }
-  __shared__ int sw[PART_THREADS / 32];
   if (lane == 31) sw[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long agg[1] = {0}, excl[1];
+    for (int q = 0; q < PART_THREADS / 32; ++q) agg[0] += sw[q];
+    lb_prefix<1>(lbs, t, agg, excl, head);
+    if (lane == 0) s_excl = excl[0];
+  }
   __syncthreads();
   int wpre = 0;
   for (int q = 0; q < w; ++q) wpre += sw[q];
-  int lp = tile_pre[t] + wpre + incl - c;   // left elements of this segment before `base`
+  int lp = (int)s_excl + wpre + incl - c;   // left elements of this segment before `base`
 #pragma unroll
   for (int q = 0; q < PART_ITEMS; ++q) {
-    int i = base + q;
+    const int i = base + q;
     if (i < tend) {
-      int dst = f[q] ? s0 + lp : s0 + k + (i - s0) - lp;
+      const int dst = f[q] ? s0 + lp : s0 + k + (i - s0) - lp;
       D[dst] = e[q];
       lp += f[q];
     }
@@ -435,7 +377,6 @@ k_subtree(SubArgs A, DevStatus* st) {
   int* q_cr = q_k + nseg_max;
   int* q_P = q_cr + nseg_max;
   unsigned char* q_ax = reinterpret_cast<unsigned char*>(q_P + nseg_max);
-  __shared__ int s_warp[SUB_THREADS / 32];
 
   {
     const int2* X = A.xpar[j0] ? A.X1 : A.X0;
@@ -448,9 +389,17 @@ k_subtree(SubArgs A, DevStatus* st) {
   }
   __syncthreads();
 
-  const int chunk = (n + SUB_THREADS - 1) / SUB_THREADS;
-  const int c0 = min(n, (int)threadIdx.x * chunk), c1 = min(n, c0 + chunk);
+  // every warp owns a contiguous, 32-aligned element range; lanes take
+  // consecutive elements (coalesced, bank-conflict-free SMEM) and the stable
+  // partition positions come from ballots: prefix = warp base + popc(lower lanes)
+  constexpr int NW = SUB_THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wchunk = ((n + NW - 1) / NW + 31) & ~31;
+  const int w0 = min(n, w * wchunk), w1 = min(n, w0 + wchunk);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  __shared__ int s_wpre[NW];
+  int* q_loc = q_P;                      // per segment: local prefix at its start ...
+  unsigned char* q_w = reinterpret_cast<unsigned char*>(q_ax + nseg_max);  // ... and its warp
 
   for (int s = A.sb; s < A.S; ++s) {
     const int nloc = 1 << (s - A.sb);
@@ -470,47 +419,57 @@ k_subtree(SubArgs A, DevStatus* st) {
       q_ax[q] = along_y;
     }
     __syncthreads();
-    // pass 1: count flags of this thread's contiguous chunk
-    int c = 0;
-    for (int i = c0; i < c1; ++i) {
-      int q = segid[i];
-      bool ay = q_ax[q];
-      c += part_flag(ay ? sx[i] : sy[i], ay, q_cr[q]);
+    // pass 1: flags of the moving copy; record the in-warp prefix at segment starts
+    int run = 0;
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+      const int i = i0 + lane;
+      bool f = false;
+      int q = 0;
+      if (i < w1) {
+        q = segid[i];
+        const bool ay = q_ax[q];
+        f = part_flag(ay ? sx[i] : sy[i], ay, q_cr[q]);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (i < w1 && q_s0[q] == i) {
+        q_loc[q] = run + __popc(bal & lt_mask);
+        q_w[q] = (unsigned char)w;
+      }
+      run += __popc(bal);
     }
-    int incl = c;
-    for (int d = 1; d < 32; d <<= 1) {
-      int o = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += o;
-    }
-    if (lane == 31) s_warp[w] = incl;
+    if (lane == 0) s_wpre[w] = run;
     __syncthreads();
-    int pre = incl - c;
-    for (int q = 0; q < w; ++q) pre += s_warp[q];
-    // pass 2: prefix at every segment start
-    {
-      int P = pre;
-      for (int i = c0; i < c1; ++i) {
-        int q = segid[i];
-        if (q_s0[q] == i) q_P[q] = P;
-        bool ay = q_ax[q];
-        P += part_flag(ay ? sx[i] : sy[i], ay, q_cr[q]);
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int q = 0; q < NW; ++q) {
+        const int v = s_wpre[q];
+        s_wpre[q] = acc;
+        acc += v;
       }
     }
     __syncthreads();
-    // pass 3: scatter the moving copy into scratch
-    {
-      int P = pre;
-      for (int i = c0; i < c1; ++i) {
-        int q = segid[i];
-        bool ay = q_ax[q];
-        int2 e = ay ? sx[i] : sy[i];
-        bool f = part_flag(e, ay, q_cr[q]);
-        int lp = P - q_P[q];
-        int s0 = q_s0[q];
-        int dst = f ? s0 + lp : s0 + q_k[q] + (i - s0) - lp;
-        scr[dst] = e;
-        P += f;
+    for (int q = threadIdx.x; q < nloc; q += blockDim.x) q_loc[q] += s_wpre[q_w[q]];
+    __syncthreads();
+    // pass 2: scatter the moving copy into scratch (stable in both halves)
+    run = s_wpre[w];
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+      const int i = i0 + lane;
+      bool f = false;
+      int q = 0;
+      int2 e = make_int2(0, 0);
+      if (i < w1) {
+        q = segid[i];
+        const bool ay = q_ax[q];
+        e = ay ? sx[i] : sy[i];
+        f = part_flag(e, ay, q_cr[q]);
       }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (i < w1) {
+        const int lp = run + __popc(bal & lt_mask) - q_loc[q];   // left elements of q before i
+        const int s0 = q_s0[q];
+        scr[f ? s0 + lp : s0 + q_k[q] + (i - s0) - lp] = e;
+      }
+      run += __popc(bal);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -655,7 +614,7 @@ void radix_sort_pairs(DBuf& tmp, const K* kin, K* kout, const V* vin, V* vout, l
 }
 
 int smem_need(long long nmax, int nseg) {
-  return (int)(3 * 8 * nmax + 2 * ((nmax + 1) & ~1ll) + 17ll * nseg + 64);
+  return (int)(3 * 8 * nmax + 2 * ((nmax + 1) & ~1ll) + 18ll * nseg + 64);
 }
 
 }  // namespace
@@ -808,7 +767,6 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
     const long long pmax = (1ll << std::max(sb, 1)) + 2;
     for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
-    T.cutrank.reserve(sizeof(int) * pmax + pmax);
     note_launch();
     k_init_arrays<<<nblk(n, 256), 256, 0, st>>>(n, T.perm_x.as<int>(), T.perm_y.as<int>(),
                                                 T.rank_x.as<int>(), T.rank_y.as<int>(),
@@ -820,31 +778,32 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                L, spec.s0, spec.seg};
     unsigned char *xp = T.xpar0.as<unsigned char>(), *yp = T.ypar0.as<unsigned char>();
     unsigned char *xq = T.xpar1.as<unsigned char>(), *yq = T.ypar1.as<unsigned char>();
-    int* cutrank = T.cutrank.as<int>();
-    unsigned char* axis_cur = reinterpret_cast<unsigned char*>(cutrank + pmax);
     int maxtiles = 1;
     for (int s = 0; s < sb; ++s) maxtiles = std::max(maxtiles, P.tile_count[s]);
-    T.tile_cnt.reserve(sizeof(int) * maxtiles);
-    T.tile_pre.reserve(sizeof(int) * maxtiles);
     const int2 *X0 = T.X0.as<int2>(), *X1 = T.X1.as<int2>(), *Y0 = T.Y0.as<int2>(),
                *Y1 = T.Y1.as<int2>();
+    // look-back state of the fused step kernel (grow-only, epoch-tagged)
+    if (T.lb_tiles < maxtiles + 1) {
+      T.lb_flags.reserve(sizeof(unsigned) * (maxtiles + 1));
+      T.lb_vals.reserve(sizeof(long long) * 2 * (maxtiles + 1));
+      T.lb_ticket.reserve(sizeof(unsigned) * 4);
+      FMM_CUDA(cudaMemsetAsync(T.lb_flags.p, 0, sizeof(unsigned) * (maxtiles + 1), st));
+      FMM_CUDA(cudaMemsetAsync(T.lb_ticket.p, 0, sizeof(unsigned) * 4, st));
+      T.lb_tiles = maxtiles + 1;
+    }
     for (int s = 0; s < sb; ++s) {
-      note_launch();
-      k_global_prepare<<<nblk(1ll << s, 128), 128, 0, st>>>(a, s, X0, X1, Y0, Y1, xp, yp, xq, yq,
-                                                           cutrank, axis_cur, dstat);
       const int nt = P.tile_count[s];
       const int* tseg = P.d_tile_seg.as<int>() + P.tile_base[s];
       const int* tstart = P.d_tile_start.as<int>() + P.tile_base[s];
+      T.lb_epoch = (T.lb_epoch + 1) & 0x3fffffffu;
+      if (T.lb_epoch == 0) T.lb_epoch = 1;
+      long long* v = T.lb_vals.as<long long>();
+      const LookbackState lbs{T.lb_flags.as<unsigned>(), v, v + T.lb_tiles,
+                              T.lb_ticket.as<unsigned>(), T.lb_epoch};
       note_launch();
-      k_part_count<<<nt, PART_THREADS, 0, st>>>(s, tseg, tstart, P.d_off.as<int>(), X0, X1, Y0,
-                                                Y1, xp, yp, cutrank, axis_cur,
-                                                T.tile_cnt.as<int>());
-      note_launch();
-      k_part_scan<<<1, 1024, 0, st>>>(nt, tseg, T.tile_cnt.as<int>(), T.tile_pre.as<int>());
-      note_launch();
-      k_part_scatter<<<nt, PART_THREADS, 0, st>>>(
-          s, tseg, tstart, P.d_off.as<int>(), T.X0.as<int2>(), T.X1.as<int2>(), T.Y0.as<int2>(),
-          T.Y1.as<int2>(), xp, yp, cutrank, axis_cur, T.tile_pre.as<int>());
+      k_part_step<<<nt, PART_THREADS, 0, st>>>(a, s, tseg, tstart, T.X0.as<int2>(),
+                                               T.X1.as<int2>(), T.Y0.as<int2>(), T.Y1.as<int2>(),
+                                               xp, yp, xq, yq, lbs, (unsigned)nt, dstat);
       std::swap(xp, xq);
       std::swap(yp, yq);
     }
