@@ -154,6 +154,30 @@ __device__ __forceinline__ bool well_separated_swapped(double ra, double rb, dou
   return __dadd_rn(small, __dmul_rn(theta, big)) <= __dmul_rn(theta, d);
 }
 
+// Same predicates from the centre difference (dx, dy), with a cheap filter:
+// lhs^2 against theta^2 (dx^2 + dy^2) decides unless the two agree to 2^-40
+// relative (the filter's rounding error is < 2^-50, the exact path's d and
+// theta*d are within 3 ulp of theta |dz|), so only near-boundary cases pay for
+// the bit-exact IEEE division and square root of numpy_cabs.  Overflow,
+// underflow or NaN in the squares fall through to the exact path.
+__device__ __forceinline__ bool theta_test(double lhs, double dx, double dy, double theta) {
+  const double l2 = lhs * lhs;
+  const double r2 = (theta * theta) * fma(dx, dx, dy * dy);
+  if (l2 < r2 * (1.0 - 0x1p-40)) return true;
+  if (l2 > r2 * (1.0 + 0x1p-40)) return false;
+  return lhs <= __dmul_rn(theta, numpy_cabs(dx, dy));
+}
+__device__ __forceinline__ bool well_separated_dz(double ra, double rb, double dx, double dy,
+                                                  double theta) {
+  const double big = fmax(ra, rb), small = fmin(ra, rb);
+  return theta_test(__dadd_rn(big, __dmul_rn(theta, small)), dx, dy, theta);
+}
+__device__ __forceinline__ bool well_separated_swapped_dz(double ra, double rb, double dx,
+                                                          double dy, double theta) {
+  const double big = fmax(ra, rb), small = fmin(ra, rb);
+  return theta_test(__dadd_rn(small, __dmul_rn(theta, big)), dx, dy, theta);
+}
+
 // ----------------------------------------------------------------------------
 // order-preserving 64-bit key of a double (-0.0 folded onto +0.0)
 __device__ __forceinline__ unsigned long long ordered_key(double v) {

@@ -90,7 +90,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
         if (!own[j]) continue;                                   // warp-uniform
         // d = |c_target - c_source| (geometry.py:40), then the θ-test (:41)
         const bool far =
-            valid && well_separated(rt[j], rc, numpy_cabs(xt[j] - xc, yt[j] - yc), theta);
+            valid && well_separated_dz(rt[j], rc, xt[j] - xc, yt[j] - yc, theta);
         const unsigned m = __ballot_sync(0xffffffffu, far);
         if (lane == 0 && (c0 >> 5) < CL_MAXM) s_mask[w][u][j][c0 >> 5] = m;
         nw[j] += __popc(m);
@@ -192,9 +192,8 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
           m = s_mask[w][u][j][c0 >> 5];
         } else {
           const long long gb = lb + 4 * P + j;
-          const bool far = valid && well_separated(geo.r[gb], rc,
-                                                   numpy_cabs(geo.cx[gb] - xc, geo.cy[gb] - yc),
-                                                   theta);
+          const bool far = valid && well_separated_dz(geo.r[gb], rc, geo.cx[gb] - xc,
+                                                      geo.cy[gb] - yc, theta);
           m = __ballot_sync(0xffffffffu, far);
         }
         const unsigned sm = vm & ~m;
@@ -238,8 +237,8 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
     src = valid ? s_idx[c] : 0;
     if (valid) {
       const double rs = geo.r[lb + src];
-      const double d = numpy_cabs(xt - geo.cx[lb + src], yt - geo.cy[lb + src]);
-      const bool sw = well_separated_swapped(rt, rs, d, theta);
+      const bool sw = well_separated_swapped_dz(rt, rs, xt - geo.cx[lb + src],
+                                                yt - geo.cy[lb + src], theta);
       const bool moved = sw && src != b && rs != rt;
       kind = moved ? (rs > rt ? 1 : 2) : 0;
     }

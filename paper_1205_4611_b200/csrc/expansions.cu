@@ -353,6 +353,10 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   M2LPair<PM> P;
   for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
     m2l_load_pair<PM>(P, item * M2L_ITEM + tid, npairs, w_src, w_tgt, mult, p);
+    // targets just before / after the item (segments continuing across items)
+    const int prev_t = item > 0 ? __ldg(w_tgt + item * M2L_ITEM - 1) : -1;
+    const long long nxt = (item + 1) * M2L_ITEM;
+    const int next_t = nxt < npairs ? __ldg(w_tgt + nxt) : -1;
     const bool valid = P.t >= 0;
     const int t = P.t;
     const int tt = valid ? t : 0;
@@ -414,11 +418,9 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
     __syncthreads();
     const int nseg = s_nseg;
     const int R = 2 * (p + 1);
-    const int t0 = s_t[0];
-    const bool first_cont = item > 0 && w_tgt[item * M2L_ITEM - 1] == t0;
+    const bool first_cont = item > 0 && prev_t == s_t[0];
     const int nvalid = s_seg[nseg];
-    const long long last = item * M2L_ITEM + nvalid - 1;
-    const bool last_cont = last + 1 < npairs && w_tgt[last + 1] == s_t[nvalid - 1];
+    const bool last_cont = nvalid == M2L_ITEM && next_t >= 0 && next_t == s_t[nvalid - 1];
     for (int task = tid; task < nseg * R; task += M2L_ITEM) {
       const int sg = task / R, r = task - sg * R;
       const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
