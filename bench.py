@@ -54,6 +54,53 @@ def p2p_flops_per_interaction():
     return 11
 
 
+HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)
+
+
+def hbm_peak():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback copy bandwidth"
+
+
+def phase_roofline(phase_ms, totals, n, m, levels, p, aliased, fp64_peak):
+    """Per-phase roofline fractions (SURVEY 8(d) algorithmic work per unit).
+
+    Compute phases count flops against the FP64 peak; the tree build counts
+    bytes against HBM.  Interaction counts use the uniform leaf population
+    n / 4^L (exact for the median-split tree up to +-1 per leaf)."""
+    leaves = 4 ** levels
+    per_leaf_src, per_leaf_ev = n / leaves, m / leaves
+    k_children = sum(4 ** l for l in range(2, levels + 1))
+    work = {
+        "sort": ("bytes", 2 * levels * 2 * (28 * n + (0 if aliased else 20 * m))),
+        "connect": ("bytes", 4 * sum(totals.values())),
+        "p2m": ("flop", n * (8 * p + 2) + totals["p2l"] * per_leaf_src * (8 * (p + 1) + 11)),
+        "m2m": ("flop", k_children * (p * (p - 1) + 18 * p)),
+        "m2l": ("flop", totals["weak"] * (2 * p * (p + 1) + 18 * p)),
+        "l2l": ("flop", k_children * (p * (p + 1) + 12 * p)),
+        "l2p": ("flop", m * (8 * p + 2) + totals["m2p"] * per_leaf_ev * (8 * p + 10)),
+        "p2p": ("flop", totals["p2p"] * per_leaf_ev * per_leaf_src * 11),
+    }
+    hbm, _ = hbm_peak()
+    out = {}
+    for k, (kind, w) in work.items():
+        ms = phase_ms.get(k, 0.0)
+        if ms <= 0:
+            continue
+        if kind == "flop":
+            ach = w / (ms * 1e-3) / 1e12
+            out[k] = {"bound": "fp64", "achieved": round(ach, 3), "unit": "TFLOP/s",
+                      "frac": round(ach / fp64_peak, 4)}
+        else:
+            ach = w / (ms * 1e-3) / 1e9
+            out[k] = {"bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                      "frac": round(ach / hbm, 4)}
+    return out
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -240,6 +287,8 @@ def run_ours(args, cfg, ws, rank, local):
                      "algorithmic": f"{pairs} M2L pairs x {m2l_flops_per_pair(cfg['p'])} flop "
                                     "(SURVEY 8(d)) per launch / M2L phase event time",
                      "peak_source": peak_src},
+        "phase_roofline": phase_roofline(phase_ms, last.list_totals, n, m, int(last.n_levels),
+                                         cfg["p"], alias, peak),
         "clocks": clk,
         "gpu_launches": int(last.kernel_launches) * args.steps,
         "gpu_launches_per_step": int(last.kernel_launches),

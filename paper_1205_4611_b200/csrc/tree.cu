@@ -28,10 +28,19 @@ namespace fmm {
 namespace {
 
 constexpr int PART_THREADS = 256;
-constexpr int PART_ITEMS = 8;
+#ifndef TREE_PART_ITEMS
+#define TREE_PART_ITEMS 8
+#endif
+#ifndef TREE_SUB_THREADS
+#define TREE_SUB_THREADS 512
+#endif
+#ifndef TREE_SMEM_BUDGET
+#define TREE_SMEM_BUDGET (110 * 1024)
+#endif
+constexpr int PART_ITEMS = TREE_PART_ITEMS;
 constexpr int PART_TILE = PART_THREADS * PART_ITEMS;
-constexpr int SUB_THREADS = 512;
-constexpr int SMEM_BUDGET = 110 * 1024;   // two subtree CTAs per SM
+constexpr int SUB_THREADS = TREE_SUB_THREADS;
+constexpr int SMEM_BUDGET = TREE_SMEM_BUDGET;   // two subtree CTAs per SM
 constexpr int LEAF_SMEM_MAX = 512;        // in-SMEM index sort of leaves up to this size
 
 struct Rect {
