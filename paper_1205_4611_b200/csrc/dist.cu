@@ -1070,7 +1070,7 @@ int fmm2d_dist_downward(fmm2d_ctx* c, double* d_vals, int64_t* d_idx, fmm2d_repo
     record(c, 8);
     run_l2l(T, E, dst, c->st, D.part);
     record(c, 9);
-    run_l2p_m2p(T, Ls, E, dst, c->st, D.g0, D.g0 + D.n_r);
+    run_l2p_m2p(T, Ls, E, dst, c->st, D.g0, D.g0 + D.n_r, D.part.lo(L), D.part.hi(L));
     record(c, 10);
     run_p2p(T, Ls, E, D.leaf_off.as<int>(), reinterpret_cast<double2*>(d_vals), dst, c->st,
             D.part, D.g0);

@@ -148,6 +148,7 @@ struct ExpState {
   DBuf phi;                          // double2[M] tree order
   DBuf values;                       // double2[M] input order
   DBuf partials, item_flags;         // M2L cross-warp partial sums
+  DBuf long_list;                    // leaves with long m2p lists (+ count)
 };
 
 // count of engine kernel launches (gpu_launches evidence in the report)
@@ -175,7 +176,8 @@ void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
              const Part& part = Part());
 // L2P + M2P for tree-ordered evaluation points [e0, e1) (e1 < 0: all)
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
-                 cudaStream_t st, long long e0 = 0, long long e1 = -1);
+                 cudaStream_t st, long long e0 = 0, long long e1 = -1,
+                 long long leaf_range_lo = 0, long long leaf_range_hi = 0);
 // values in input order, or (out_base >= 0) tree order starting at point out_base
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part = Part(),

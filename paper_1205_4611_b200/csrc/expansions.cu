@@ -25,6 +25,7 @@ namespace fmm {
 namespace {
 
 constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:168-169
+constexpr int M2P_INLINE = 16;   // m2p sources per point handled by k_l2p_m2p itself
 // M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
 // target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
 bool m2l_force_target() {
@@ -587,7 +588,9 @@ k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __rest
   cplx acc = c[PM];
 #pragma unroll
   for (int j = PM - 1; j >= 0; --j) acc = cadd(cmul(acc, w), c[j]);
-  for (int q = m_off[b]; q < m_off[b + 1]; ++q) {
+  // long m2p lists (clustered inputs: up to ~850 boxes) continue in k_m2p_long
+  const int qa = m_off[b], qe = min(m_off[b + 1], qa + M2P_INLINE);
+  for (int q = qa; q < qe; ++q) {
     const long long ga = lb + m_idx[q];
     const cplx u{y.x - cx[ga], y.y - cy[ga]};
     if (u.x == 0.0 && u.y == 0.0) {
@@ -604,6 +607,89 @@ k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __rest
     acc = cadd(acc, cmul(h, inv));
   }
   phi[e] = make_double2(acc.x, acc.y);
+}
+
+// M2P beyond the first M2P_INLINE sources of a leaf (engine.py:152-160): one
+// CTA per long-list leaf; thread t sums sources t, t+256, ... for every point
+// of the leaf, then a fixed SMEM tree folds the 256 partial sums per point.
+// Deterministic; the long tail of clustered inputs is spread over 256 threads
+// instead of serialising one warp.
+constexpr int M2P_LONG_THREADS = 256;
+constexpr int M2P_LONG_POINTS = 8;      // points per pass (SMEM: 8 x 256 complex)
+
+__global__ void k_m2p_find_long(long long b0, long long b1, const int* __restrict__ m_off,
+                                int* list, int* count) {
+  const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b < b1 && m_off[b + 1] - m_off[b] > M2P_INLINE) list[atomicAdd(count, 1)] = (int)b;
+}
+
+template <int PM>
+__global__ void __launch_bounds__(M2P_LONG_THREADS)
+k_m2p_long(int L, const int* __restrict__ list, const int* __restrict__ count,
+           const int* __restrict__ eoff, const double2* __restrict__ eval_pos,
+           const int* __restrict__ m_off, const int* __restrict__ m_idx,
+           const double* __restrict__ cx, const double* __restrict__ cy,
+           const double2* __restrict__ mult, double2* phi, int p, DevStatus* st) {
+  __shared__ double2 red[M2P_LONG_POINTS][M2P_LONG_THREADS];
+  if (lists_overflowed(st)) return;
+  const int n = *count;
+  const long long lb = level_base(L);
+  const int tid = threadIdx.x;
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const int b = list[it];
+    const int e0 = eoff[b], e1 = eoff[b + 1];
+    const int q0 = m_off[b] + M2P_INLINE, q1 = m_off[b + 1];
+    for (int eb = e0; eb < e1; eb += M2P_LONG_POINTS) {
+      const int np = min(M2P_LONG_POINTS, e1 - eb);
+      cplx acc[M2P_LONG_POINTS];
+      double2 y[M2P_LONG_POINTS];
+#pragma unroll
+      for (int k = 0; k < M2P_LONG_POINTS; ++k) {
+        acc[k] = cplx{0.0, 0.0};
+        y[k] = k < np ? eval_pos[eb + k] : eval_pos[eb];
+      }
+      for (int q = q0 + tid; q < q1; q += M2P_LONG_THREADS) {
+        const long long ga = lb + m_idx[q];
+        const double2* a = mult + ga * (p + 1);
+        cplx c[PM + 1];
+#pragma unroll
+        for (int j = 1; j <= PM; ++j) c[j] = ld_coef(a, j, p);
+        const double ax = cx[ga], ay = cy[ga];
+#pragma unroll
+        for (int k = 0; k < M2P_LONG_POINTS; ++k) {
+          if (k >= np) break;
+          const cplx u{y[k].x - ax, y[k].y - ay};
+          if (u.x == 0.0 && u.y == 0.0) {
+            atomicOr(&st->flags, ST_M2P_SINGULAR);
+            continue;
+          }
+          const cplx inv = crcp_fast(u);
+          cplx h = c[PM];
+#pragma unroll
+          for (int j = PM - 1; j >= 1; --j) h = cadd(cmul(h, inv), c[j]);
+          acc[k] = cadd(acc[k], cmul(h, inv));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < M2P_LONG_POINTS; ++k) red[k][tid] = make_double2(acc[k].x, acc[k].y);
+      __syncthreads();
+      for (int w = M2P_LONG_THREADS / 2; w > 0; w >>= 1) {
+        if (tid < w) {
+#pragma unroll
+          for (int k = 0; k < M2P_LONG_POINTS; ++k) {
+            const double2 u = red[k][tid], v = red[k][tid + w];
+            red[k][tid] = make_double2(u.x + v.x, u.y + v.y);
+          }
+        }
+        __syncthreads();
+      }
+      if (tid < np) {
+        const double2 f = phi[eb + tid], v = red[tid][0];
+        phi[eb + tid] = make_double2(f.x + v.x, f.y + v.y);
+      }
+      __syncthreads();
+    }
+  }
 }
 
 inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -734,7 +820,8 @@ void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
   dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::l2l(T, E, st, part); });
 }
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
-                 cudaStream_t st, long long e0, long long e1) {
+                 cudaStream_t st, long long e0, long long e1, long long leaf_range_lo,
+                 long long leaf_range_hi) {
   if (e1 < 0) e1 = T.m;
   if (T.L == 0) {   // a single box: no expansions (engine.py:257)
     FMM_CUDA(cudaMemsetAsync(E.phi.p, 0, sizeof(double2) * T.m, st));
@@ -747,6 +834,24 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
         T.m, e0, e1, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
         T.box_cx.as<double>(), T.box_cy.as<double>(), E.mult.as<double2>(),
         E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
+    // leaves of the evaluated range with long m2p lists
+    const long long nleaf = 1ll << (2 * T.L);
+    long long b0 = 0, b1 = nleaf;
+    if (e0 > 0 || e1 < T.m) {          // distributed rank: its leaves
+      b0 = leaf_range_lo;
+      b1 = leaf_range_hi;
+    }
+    E.long_list.reserve(sizeof(int) * (nleaf + 2));
+    int* cnt = E.long_list.as<int>() + nleaf;
+    FMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    note_launch();
+    k_m2p_find_long<<<nblk(b1 - b0, 256), 256, 0, st>>>(b0, b1, Ls.m2p_off.as<int>(),
+                                                        E.long_list.as<int>(), cnt);
+    note_launch();
+    k_m2p_long<decltype(pm)::value><<<2 * 148, M2P_LONG_THREADS, 0, st>>>(
+        T.L, E.long_list.as<int>(), cnt, T.eoff_t, T.epos_t, Ls.m2p_off.as<int>(),
+        Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
+        E.mult.as<double2>(), E.phi.as<double2>(), E.p, dstat);
   });
 }
 

@@ -3,7 +3,7 @@ Usage: python tools/ncu_kernel.py report.ncu-rep"""
 import csv, io, subprocess, sys
 KEYS = ['gpu__time_duration.sum', 'launch__registers_per_thread',
         'sm__warps_active.avg.pct_of_peak_sustained_active',
-        'TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed',
+        'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
         'sm__inst_executed.avg.per_cycle_active', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
         'smsp__inst_executed.sum', 'smsp__thread_inst_executed_per_inst_executed.ratio',
         'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_sector_hit_rate.pct',
