@@ -101,7 +101,7 @@ struct TreeState {
   const double* g_p = nullptr;       //   device memory), original order
   const double2* epos_p = nullptr;
   DBuf keys_in, keys_out, vals_in, vals_out, cub_tmp;
-  DBuf xs_sorted, ys_sorted, perm_x, perm_y, rank_x, rank_y;
+  DBuf perm_x, perm_y, rank_x, rank_y;
   DBuf X0, X1, Y0, Y1;               // int2 (rank_x, rank_y) arrays
   DBuf xpar0, xpar1, ypar0, ypar1, cutrank;
   DBuf tile_cnt, tile_pre;

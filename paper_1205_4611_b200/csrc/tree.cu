@@ -183,14 +183,11 @@ __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
   for (int q = 0; q < cnt; ++q) perm[i + q] = idx[q];
 }
 
-__global__ void k_rank_scatter(const double2* __restrict__ pos, long long n, int axis,
-                               const int* __restrict__ perm, double* sorted, int* rank) {
-  long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  int i = perm[r];
-  double2 z = pos[i];
-  sorted[r] = axis ? z.y : z.x;
-  rank[i] = (int)r;
+// inverse permutation: rank of every point along the sorted axis (an
+// L2-resident scatter; the coordinates are looked up only at the cuts)
+__global__ void k_rank_scatter(long long n, const int* __restrict__ perm, int* rank) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r < n) rank[perm[r]] = (int)r;
 }
 
 __global__ void k_init_arrays(long long n, const int* __restrict__ perm_x,
@@ -211,8 +208,9 @@ struct StepArgs {
   Rect* rect_tab;
   double* cut_tab;
   unsigned char* axis_tab;
-  const double* xs_sorted;
-  const double* ys_sorted;
+  const double2* pos;       // input positions (original order)
+  const int* perm_x;        // original index at every x rank
+  const int* perm_y;        // ... and y rank
   int L;
   int s0;                   // global step of local step 0 (subtree builds)
   long long seg;            // global index of the local root segment at step s0
@@ -227,8 +225,8 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
   const int sg = s + a.s0;                                          // global step
   if ((sg & 1) == 0 && (sg >> 1) < a.L) {                           // tree.py:348
-    double xa = a.xs_sorted[x_first.x], xb = a.xs_sorted[x_last.x];
-    double ya = a.ys_sorted[y_first.y], yb = a.ys_sorted[y_last.y];
+    double xa = a.pos[a.perm_x[x_first.x]].x, xb = a.pos[a.perm_x[x_last.x]].x;
+    double ya = a.pos[a.perm_y[y_first.y]].y, yb = a.pos[a.perm_y[y_last.y]].y;
     if (xa == xb && ya == yb) {
       unsigned long long key = ((unsigned long long)(sg >> 1) << 40) |
                                (unsigned long long)((a.seg << s) + j);
@@ -237,12 +235,13 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
     }
   }
   const int cr = along_y ? y_kth.y : x_kth.x;
-  const double cut = along_y ? a.ys_sorted[cr] : a.xs_sorted[cr];  // tree.py:265
+  // coordinate of rank cr along the axis (tree.py:265)
+  const double cut = along_y ? a.pos[a.perm_y[cr]].y : a.pos[a.perm_x[cr]].x;
   // evaluation points split by coord <= cut (tree.py:273): they follow the
   // sources' median split exactly unless the (k+1)-th coordinate equals the cut
   const int k = (n + 1) / 2;
   if (k < n) {
-    const double nxt = along_y ? a.ys_sorted[y_next.y] : a.xs_sorted[x_next.x];
+    const double nxt = along_y ? a.pos[a.perm_y[y_next.y]].y : a.pos[a.perm_x[x_next.x]].x;
     if (nxt == cut) atomicOr(&st->flags, ST_EVAL_TIES);
   }
   a.cut_tab[step_base(s) + j] = cut;
@@ -747,8 +746,6 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
 
   if (S > 0) {
     // global ranks along x and y (ties by original index: stable radix sort)
-    T.xs_sorted.reserve(sizeof(double) * n);
-    T.ys_sorted.reserve(sizeof(double) * n);
     for (DBuf* b : {&T.perm_x, &T.perm_y, &T.rank_x, &T.rank_y}) b->reserve(sizeof(int) * n);
     for (int axis = 0; axis < 2; ++axis) {
       int* perm = axis ? T.perm_y.as<int>() : T.perm_x.as<int>();
@@ -769,9 +766,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         k_fix_ties<<<nblk(n, 256), 256, 0, st>>>(kout, perm, pos, axis, n, dstat);
       }
       note_launch();
-      k_rank_scatter<<<nblk(n, 256), 256, 0, st>>>(
-          pos, n, axis, perm, axis ? T.ys_sorted.as<double>() : T.xs_sorted.as<double>(),
-          axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
+      k_rank_scatter<<<nblk(n, 256), 256, 0, st>>>(n, perm, axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
     }
     for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
     const long long pmax = (1ll << std::max(sb, 1)) + 2;
@@ -783,7 +778,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                                                 T.xpar0.as<unsigned char>(),
                                                 T.ypar0.as<unsigned char>());
     StepArgs a{P.d_off.as<int>(), T.rect_tab.as<Rect>(), T.cut_tab.as<double>(),
-               T.axis_tab.as<unsigned char>(), T.xs_sorted.as<double>(), T.ys_sorted.as<double>(),
+               T.axis_tab.as<unsigned char>(), pos, T.perm_x.as<int>(), T.perm_y.as<int>(),
                L, spec.s0, spec.seg};
     unsigned char *xp = T.xpar0.as<unsigned char>(), *yp = T.ypar0.as<unsigned char>();
     unsigned char *xq = T.xpar1.as<unsigned char>(), *yq = T.ypar1.as<unsigned char>();
