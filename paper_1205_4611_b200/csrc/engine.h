@@ -149,6 +149,7 @@ struct ExpState {
   DBuf values;                       // double2[M] input order
   DBuf partials, item_flags;         // M2L cross-warp partial sums
   DBuf long_list;                    // leaves with long m2p lists (+ count)
+  DBuf p2l_rows;                     // one P2L row per p2l pair
 };
 
 // count of engine kernel launches (gpu_launches evidence in the report)

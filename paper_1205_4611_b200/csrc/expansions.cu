@@ -92,50 +92,73 @@ k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
     if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
 }
 
-// P2L (engine.py:85-93, operators.py:209-224): one thread per target leaf;
-// b_k += sum_i g_i w_i^(k+1), w_i = 1/(z_i - z0), over the particles of its
-// p2l source leaves in ascending order.  P2L lists are short (~1 source leaf
-// per target), so a thread's sequential power chain is cheaper than any
-// cross-lane reduction of the (p+1)-term rows.
+// P2L (engine.py:85-93, operators.py:209-224) in two balanced steps:
+//  k_p2l_pair: one thread per (target leaf, p2l source leaf) pair computes the
+//    pair's row sum_i g_i w_i^(k+1), w_i = 1/(z_i - z0), over the source leaf's
+//    particles (what one ops.p2l call returns);
+//  k_p2l_fold: one thread per target leaf adds its pairs' rows in ascending
+//    source order (the reference's local[b] += ... sequence) and initialises
+//    local[L] (zero without p2l sources).
 template <int PM>
 __global__ void __launch_bounds__(128)
-k_p2l(int L, long long b0, long long b1, const int* __restrict__ offL,
-      const int* __restrict__ l_off, const int* __restrict__ l_idx,
-      const double2* __restrict__ src_pos, const double* __restrict__ src_g,
-      const double* __restrict__ cx, const double* __restrict__ cy, double2* local, int p,
-      DevStatus* st) {
-  const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (b >= b1 || lists_overflowed(st)) return;
+k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
+           const int* __restrict__ l_off, const int* __restrict__ l_idx,
+           const double2* __restrict__ src_pos, const double* __restrict__ src_g,
+           const double* __restrict__ cx, const double* __restrict__ cy, double2* rows, int p,
+           DevStatus* st) {
+  if (lists_overflowed(st)) return;
   const long long lb = level_base(L);
-  double2* out = local + (lb + b) * (p + 1);
-  const int q0 = l_off[b], q1 = l_off[b + 1];
-  cplx acc[PM + 1];
-#pragma unroll
-  for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
-  if (q0 < q1) {
+  const int qbase = l_off[b0], qend = l_off[b1];
+  for (long long q = qbase + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < qend;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long lo = b0, hi = b1;                 // target: l_off[b] <= q < l_off[b+1]
+    while (hi - lo > 1) {
+      const long long mid = (lo + hi) >> 1;
+      if (l_off[mid] <= q) lo = mid; else hi = mid;
+    }
+    const long long b = lo;
     const double x0 = cx[lb + b], y0 = cy[lb + b];
-    for (int q = q0; q < q1; ++q) {
-      const int a = l_idx[q];
-      for (int i = offL[a]; i < offL[a + 1]; ++i) {
-        const double2 z = src_pos[i];
-        const cplx d{z.x - x0, z.y - y0};
-        if (d.x == 0.0 && d.y == 0.0) {
-          atomicOr(&st->flags, ST_P2L_SINGULAR);
-          continue;
-        }
-        const cplx inv = crcp_fast(d);
-        cplx w = cscale(inv, src_g[i]);
+    const int a = l_idx[q];
+    cplx acc[PM + 1];
 #pragma unroll
-        for (int k = 0; k <= PM; ++k) {
-          acc[k] = cadd(acc[k], w);
-          w = cmul(w, inv);
-        }
+    for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
+    for (int i = offL[a]; i < offL[a + 1]; ++i) {
+      const double2 z = src_pos[i];
+      const cplx d{z.x - x0, z.y - y0};
+      if (d.x == 0.0 && d.y == 0.0) {
+        atomicOr(&st->flags, ST_P2L_SINGULAR);
+        continue;
+      }
+      const cplx inv = crcp_fast(d);
+      cplx w = cscale(inv, src_g[i]);
+#pragma unroll
+      for (int k = 0; k <= PM; ++k) {
+        acc[k] = cadd(acc[k], w);
+        w = cmul(w, inv);
       }
     }
-  }
+    double2* out = rows + (q - qbase) * (p + 1);
 #pragma unroll
-  for (int j = 0; j <= PM; ++j)
-    if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
+    for (int j = 0; j <= PM; ++j)
+      if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_p2l_fold(int L, long long b0, long long b1, const int* __restrict__ l_off,
+           const double2* __restrict__ rows, double2* local, int p, DevStatus* st) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long b = b0 + t / (p + 1);
+  const int j = (int)(t % (p + 1));
+  if (b >= b1 || lists_overflowed(st)) return;
+  const int qbase = l_off[b0];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = l_off[b]; q < l_off[b + 1]; ++q) {
+    const double2 v = rows[(long long)(q - qbase) * (p + 1) + j];
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  local[(level_base(L) + b) * (p + 1) + j] = acc;
 }
 
 // --------------------------------------------------------------------------
@@ -707,10 +730,15 @@ struct Launch {
                                                   T.src_g.as<double>(), T.box_cx.as<double>(),
                                                   T.box_cy.as<double>(), E.mult.as<double2>(), p);
     note_launch();
-    k_p2l<PM><<<nblk(b1 - b0, 128), 128, 0, st>>>(
+    E.p2l_rows.reserve(sizeof(double2) * std::max(1ll, Ls.cap_p2l) * (p + 1));
+    k_p2l_pair<PM><<<8 * sm_count(), 128, 0, st>>>(
         L, b0, b1, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
-        E.local.as<double2>(), p, dstat);
+        E.p2l_rows.as<double2>(), p, dstat);
+    note_launch();
+    k_p2l_fold<<<nblk((b1 - b0) * (p + 1), 128), 128, 0, st>>>(
+        L, b0, b1, Ls.p2l_off.as<int>(), E.p2l_rows.as<double2>(), E.local.as<double2>(), p,
+        dstat);
   }
   static void m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part, int lmin,
                   int lmax) {
