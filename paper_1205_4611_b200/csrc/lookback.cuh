@@ -91,3 +91,64 @@ __device__ __forceinline__ void lb_prefix(const LookbackState& S, unsigned tile,
 }
 
 }  // namespace fmm
+
+namespace fmm {
+
+// Single-counter variant with the flag and the value packed in one 64-bit
+// word (2-bit state | 30-bit epoch tag | 32-bit value): one load per window
+// lane and no fence between value and flag, halving the latency of every
+// look-back step.  Values (and prefixes) must fit in 32 bits.
+struct LookbackPacked {
+  unsigned long long* word;   // [ntiles]
+  unsigned* ticket;
+  unsigned epoch;             // nonzero, < 2^30
+};
+
+__device__ __forceinline__ unsigned lb_ticket(const LookbackPacked& S, unsigned ntiles) {
+  const unsigned t = atomicAdd(S.ticket, 1u);
+  if (t == ntiles - 1) atomicExch(S.ticket, 0u);
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long lb_pack(unsigned epoch, unsigned state,
+                                                      unsigned value) {
+  return ((unsigned long long)((epoch << 2) | state) << 32) | value;
+}
+
+// called by one full warp; returns the exclusive prefix of `agg` over the
+// tiles of the current chain (a chain starts at tile 0 or a `head` tile)
+__device__ __forceinline__ unsigned lb_prefix_packed(const LookbackPacked& S, unsigned tile,
+                                                     unsigned agg, bool head) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0 || head) {
+    if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 2u, agg));
+    __syncwarp();
+    return 0;
+  }
+  if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 1u, agg));
+  unsigned excl = 0;
+  long long top = (long long)tile - 1;
+  while (true) {
+    const long long p = top - lane;
+    unsigned long long v = lb_pack(S.epoch, 2u, 0u);   // lanes past tile 0: terminator
+    if (p >= 0) {
+      do {
+        v = *(volatile unsigned long long*)(S.word + p);
+      } while ((unsigned)(v >> 34) != S.epoch || ((v >> 32) & 3u) == 0);
+    }
+    const unsigned st = (unsigned)(v >> 32) & 3u;
+    const unsigned inc = __ballot_sync(0xffffffffu, st == 2u);
+    const int stop = inc ? __ffs(inc) - 1 : 31;
+    unsigned x = lane <= stop ? (unsigned)v : 0u;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+    excl += x;
+    if (inc) break;
+    top -= 32;
+  }
+  if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 2u, excl + agg));
+  __syncwarp();
+  return excl;
+}
+
+}  // namespace fmm

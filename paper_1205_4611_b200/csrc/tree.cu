@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(PART_THREADS)
 k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
             const int* __restrict__ tile_start, int2* X0, int2* X1, int2* Y0, int2* Y1,
             const unsigned char* xpar, const unsigned char* ypar, unsigned char* xpar_next,
-            unsigned char* ypar_next, LookbackState lbs, unsigned ntiles, DevStatus* st) {
+            unsigned char* ypar_next, LookbackPacked lbs, unsigned ntiles, DevStatus* st) {
   __shared__ unsigned s_tile;
   __shared__ int sw[PART_THREADS / 32];
   __shared__ long long s_excl;
@@ -327,10 +327,10 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
   if (lane == 31) sw[w] = incl;
   __syncthreads();
   if (w == 0) {
-    long long agg[1] = {0}, excl[1];
-    for (int q = 0; q < PART_THREADS / 32; ++q) agg[0] += sw[q];
-    lb_prefix<1>(lbs, t, agg, excl, head);
-    if (lane == 0) s_excl = excl[0];
+    unsigned agg = 0;
+    for (int q = 0; q < PART_THREADS / 32; ++q) agg += sw[q];
+    const unsigned excl = lb_prefix_packed(lbs, t, agg, head);
+    if (lane == 0) s_excl = excl;
   }
   __syncthreads();
   int wpre = 0;
@@ -788,10 +788,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                *Y1 = T.Y1.as<int2>();
     // look-back state of the fused step kernel (grow-only, epoch-tagged)
     if (T.lb_tiles < maxtiles + 1) {
-      T.lb_flags.reserve(sizeof(unsigned) * (maxtiles + 1));
-      T.lb_vals.reserve(sizeof(long long) * 2 * (maxtiles + 1));
+      T.lb_vals.reserve(sizeof(unsigned long long) * (maxtiles + 1));
       T.lb_ticket.reserve(sizeof(unsigned) * 4);
-      FMM_CUDA(cudaMemsetAsync(T.lb_flags.p, 0, sizeof(unsigned) * (maxtiles + 1), st));
+      FMM_CUDA(cudaMemsetAsync(T.lb_vals.p, 0, sizeof(unsigned long long) * (maxtiles + 1), st));
       FMM_CUDA(cudaMemsetAsync(T.lb_ticket.p, 0, sizeof(unsigned) * 4, st));
       T.lb_tiles = maxtiles + 1;
     }
@@ -801,9 +800,8 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       const int* tstart = P.d_tile_start.as<int>() + P.tile_base[s];
       T.lb_epoch = (T.lb_epoch + 1) & 0x3fffffffu;
       if (T.lb_epoch == 0) T.lb_epoch = 1;
-      long long* v = T.lb_vals.as<long long>();
-      const LookbackState lbs{T.lb_flags.as<unsigned>(), v, v + T.lb_tiles,
-                              T.lb_ticket.as<unsigned>(), T.lb_epoch};
+      const LookbackPacked lbs{T.lb_vals.as<unsigned long long>(), T.lb_ticket.as<unsigned>(),
+                               T.lb_epoch};
       note_launch();
       k_part_step<<<nt, PART_THREADS, 0, st>>>(a, s, tseg, tstart, T.X0.as<int2>(),
                                                T.X1.as<int2>(), T.Y0.as<int2>(), T.Y1.as<int2>(),
