@@ -502,10 +502,9 @@ k_subtree(SubArgs A, DevStatus* st) {
       const int me = sidx[i];
       int rank = 0;
       for (int t = l0; t < l1; ++t) rank += sidx[t] < me;
-      const long long dst = A.out0 + g0 + l0 + rank;
-      A.src_perm[dst] = A.orig ? A.orig[me] : me;
-      A.src_pos[dst] = A.pos[me];
-      A.src_g[dst] = A.g[me];
+      // canonical position of local point `me`; the point data itself is
+      // gathered afterwards by a full-occupancy kernel (k_gather_points)
+      A.leaf_of[g0 + l0 + rank] = me;
     }
   } else {
     for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -819,6 +818,14 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
                                     P.smem_bytes));
       note_launch();
       k_subtree<<<(unsigned)(1ll << sb), SUB_THREADS, P.smem_bytes, st>>>(A, dstat);
+      if (!P.global_leaf_finalize) {
+        note_launch();
+        k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.leaf_of.as<int>(), n, pos, T.g_p,
+                                                      T.src_pos.as<double2>(),
+                                                      T.src_g.as<double>(),
+                                                      T.src_perm.as<int>(), spec.out0,
+                                                      spec.orig);
+      }
     } else {
       // every split ran as a global step: leaves are segments of the global copies
       note_launch();
