@@ -45,6 +45,16 @@ __device__ __forceinline__ bool lists_overflowed(const DevStatus* st) {
   return (*(volatile const int*)&st->flags) & ST_OVERFLOW;
 }
 
+// Programmatic dependent launch: every engine kernel is launched with the
+// PDL attribute (engine.h launch()).  It first waits for the preceding grid of
+// the stream to complete (full memory visibility, the same dependency as a
+// plain launch) and then lets the next kernel's blocks be scheduled, so the
+// launch latency of each kernel overlaps the tail of the previous one.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ----------------------------------------------------------------------------
 // complex double in registers
 struct cplx {

@@ -47,6 +47,7 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
            const int* __restrict__ ps_idx, int* so, int* sidx, long long scap, int* woff,
            int* widx, int* wtgt, long long wcap, LookbackState lbs, unsigned ntiles,
            long long P0, long long P1, long long tb, long long te, DevStatus* st) {
+  pdl_enter();
   __shared__ unsigned s_mask[CL_WARPS][CL_PPW][4][CL_MAXM];
   __shared__ int s_cnt[CL_WARPS][CL_PPW][4][2];
   __shared__ long long s_excl[2];
@@ -219,6 +220,7 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
              int* o_p2l, int* i_p2l, long long cap_p2l, int* o_m2p, int* i_m2p,
              long long cap_m2p, LookbackState lbs, unsigned ntiles, long long tb, long long te,
              DevStatus* st) {
+  pdl_enter();
   __shared__ unsigned s_mask[CL_WARPS][CL_TPW][2][CL_MAXM];   // p2l, m2p (p2p = rest)
   __shared__ int s_cnt[CL_WARPS][CL_TPW][3];
   __shared__ long long s_excl[3];
@@ -345,6 +347,7 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
 
 // off[i] for i outside the written window [lo, hi]: off[lo] before, off[hi] after
 __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > n) return;
   if (i < lo) off[i] = off[lo];
@@ -352,6 +355,7 @@ __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
 }
 
 __global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx) {
+  pdl_enter();
   weak_off[0] = 0;
   weak_off[1] = 0;     // the root has no far field (connectivity.py:106)
   s_off[0] = 0;
@@ -360,6 +364,7 @@ __global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx) {
 }
 
 __global__ void k_radius(const double* hw, const double* hh, double* r, long long n) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) r[i] = glibc_hypot(hw[i], hh[i]);
 }
@@ -369,6 +374,7 @@ __global__ void k_radius(const double* hw, const double* hh, double* r, long lon
 // global add per non-empty bin
 __global__ void __launch_bounds__(256)
 k_histogram(const int* __restrict__ off, long long n, int kind, int* hist, DevStatus* st) {
+  pdl_enter();
   __shared__ int sh[HIST_BINS];
   __shared__ int smax;
   if (lists_overflowed(st)) return;
@@ -400,7 +406,7 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 void compute_radius(TreeState& T, cudaStream_t st) {
   const long long nbox = level_base(T.L + 1);
   note_launch();
-  k_radius<<<nblk(nbox, 256), 256, 0, st>>>(T.box_hw.as<double>(), T.box_hh.as<double>(),
+  launch(k_radius, nblk(nbox, 256), 256, 0, st, T.box_hw.as<double>(), T.box_hh.as<double>(),
                                             T.box_r.as<double>(), nbox);
 }
 
@@ -449,14 +455,14 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
   int* woff = Ls.weak_off.as<int>();
   note_launch();
-  k_root_lists<<<1, 1, 0, st>>>(woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
+  launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
     const long long tb = part.lo(l), te = part.hi(l);
     const long long P0 = tb >> 2, P1 = (te + 3) >> 2;
     const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
     note_launch();
-    k_classify<<<ntiles, CL_WARPS * 32, 0, st>>>(
+    launch(k_classify, ntiles, CL_WARPS * 32, 0, st, 
         l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
         Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
         Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, P0, P1,
@@ -467,7 +473,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const long long tb = part.lo(L), te = part.hi(L);
     const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
     note_launch();
-    k_reclassify<<<ntiles, CL_WARPS * 32, 0, st>>>(
+    launch(k_reclassify, ntiles, CL_WARPS * 32, 0, st, 
         L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),
         Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
         Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles,
@@ -477,12 +483,12 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     // empty lists for boxes this rank does not own: monotone CSR offsets
     for (int l = 1; l <= L; ++l) {
       note_launch();
-      k_csr_pad<<<nblk((1ll << (2 * l)) + 1, 256), 256, 0, st>>>(woff + level_base(l), 1ll << (2 * l),
+      launch(k_csr_pad, nblk((1ll << (2 * l)) + 1, 256), 256, 0, st, woff + level_base(l), 1ll << (2 * l),
                                                            part.lo(l), part.hi(l));
     }
     for (DBuf* o : {&Ls.p2p_off, &Ls.p2l_off, &Ls.m2p_off}) {
       note_launch();
-      k_csr_pad<<<nblk(nleaf + 1, 256), 256, 0, st>>>(o->as<int>(), nleaf, part.lo(L), part.hi(L));
+      launch(k_csr_pad, nblk(nleaf + 1, 256), 256, 0, st, o->as<int>(), nleaf, part.lo(L), part.hi(L));
     }
   }
 }
@@ -496,7 +502,7 @@ void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t
   auto hist = [&](const int* off, long long n, int kind) {
     if (n <= 0) return;
     note_launch();
-    k_histogram<<<std::min(nblk(n, 256), 296u), 256, 0, st>>>(off, n, kind, Ls.hist.as<int>(),
+    launch(k_histogram, std::min(nblk(n, 256), 296u), 256, 0, st, off, n, kind, Ls.hist.as<int>(),
                                                               dstat);
   };
   if (part.G == 1) {

@@ -62,6 +62,7 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 __global__ void k_rec_load(long long n, const double2* __restrict__ pos,
                            const double* __restrict__ g, long long idx_base, Rec* rec,
                            unsigned long long* bbkeys) {
+  pdl_enter();
   double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -90,6 +91,7 @@ __device__ __forceinline__ double key_to_double(unsigned long long k) {
 }
 
 __global__ void k_bbox_out(const unsigned long long* bbkeys, double* out4) {
+  pdl_enter();
   if (threadIdx.x < 4) out4[threadIdx.x] = key_to_double(bbkeys[threadIdx.x]);
 }
 
@@ -103,6 +105,7 @@ struct SelState {
 };
 
 __global__ void k_sel_init(SelState* sel, const long long* __restrict__ kth, int nseg) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < nseg) sel[j] = SelState{0ull, kth[j], 0};
 }
@@ -116,6 +119,7 @@ __device__ __forceinline__ unsigned long long rec_key(const Rec& r, bool along_y
 __global__ void __launch_bounds__(256)
 k_sel_hist(int rho, int nseg, const Rec* __restrict__ rec, const long long* __restrict__ seg_off,
            const unsigned char* __restrict__ axis, const SelState* __restrict__ sel, int* hist) {
+  pdl_enter();
   __shared__ int sh[4][256];
   for (int i = threadIdx.x; i < nseg * 256; i += blockDim.x) sh[i >> 8][i & 255] = 0;
   __syncthreads();
@@ -137,6 +141,7 @@ k_sel_hist(int rho, int nseg, const Rec* __restrict__ rec, const long long* __re
 // pick the digit holding the k_rem-th key (same result on every rank: the
 // histogram is the allreduced one)
 __global__ void k_sel_pick(int rho, int nseg, const int* __restrict__ hist, SelState* sel) {
+  pdl_enter();
   const int j = threadIdx.x;
   if (j >= nseg) return;
   const int shift = 56 - 8 * rho;
@@ -159,6 +164,7 @@ __global__ void k_eq_count(int nseg, const Rec* __restrict__ rec,
                            const long long* __restrict__ seg_off,
                            const unsigned char* __restrict__ axis, const SelState* __restrict__ sel,
                            int* eq_local, int* eqflag) {
+  pdl_enter();
   const long long n = seg_off[nseg];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -177,6 +183,7 @@ __global__ void k_side_keys(int nseg, int G, int rank, const Rec* __restrict__ r
                             const unsigned char* __restrict__ axis,
                             const SelState* __restrict__ sel, const int* __restrict__ eq_all,
                             const int* __restrict__ eqpre, unsigned* skey, int* sval) {
+  pdl_enter();
   const long long n = seg_off[nseg];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -197,12 +204,14 @@ __global__ void k_side_keys(int nseg, int G, int rank, const Rec* __restrict__ r
 
 __global__ void k_rec_gather(long long n, const int* __restrict__ perm, const Rec* __restrict__ in,
                              Rec* out) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[perm[i]];
 }
 
 __global__ void k_seg_bounds(long long n, int nseg2, const unsigned* __restrict__ skey,
                              long long* seg_off) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > n) return;
   const long long prev = i == 0 ? -1 : (long long)skey[i - 1];
@@ -213,6 +222,7 @@ __global__ void k_seg_bounds(long long n, int nseg2, const unsigned* __restrict_
 // per-segment local bounding box for the top-level degenerate check
 __global__ void k_seg_box(int nseg, const Rec* __restrict__ rec,
                           const long long* __restrict__ seg_off, unsigned long long* keys) {
+  pdl_enter();
   const long long n = seg_off[nseg];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -227,12 +237,14 @@ __global__ void k_seg_box(int nseg, const Rec* __restrict__ rec,
 }
 
 __global__ void k_keys_out(const unsigned long long* keys, double* out, int n) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = key_to_double(keys[i]);
 }
 
 __global__ void k_rec_unpack(long long n, const Rec* __restrict__ rec, double2* pos, double* g,
                              int* idx) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Rec r = rec[i];
@@ -259,6 +271,7 @@ __device__ __forceinline__ void own_slot(long long u, int ltop, int s0, int* l_o
 __global__ void k_geo_pack(long long count, int ltop, int s0, int rank, const double* cx,
                            const double* cy, const double* hw, const double* hh,
                            const double* r, double* out) {
+  pdl_enter();
   const long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (u >= count) return;
   int l;
@@ -271,6 +284,7 @@ __global__ void k_geo_pack(long long count, int ltop, int s0, int rank, const do
 
 __global__ void k_geo_unpack(long long count, int G, int ltop, int s0, const double* in,
                              double* cx, double* cy, double* hw, double* hh, double* r) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= count * G) return;
   const int q = (int)(v / count);
@@ -300,6 +314,7 @@ __device__ __forceinline__ int owner_of(long long gid, int s0) {   // -1: shared
 
 __global__ void k_mark_weak(const int* __restrict__ total, const int* __restrict__ w_src,
                             int s0, int rank, unsigned char* flags) {
+  pdl_enter();
   const long long n = *total;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -313,6 +328,7 @@ __global__ void k_mark_weak(const int* __restrict__ total, const int* __restrict
 __global__ void k_mark_leaf_lists(long long b0, long long b1, const int* __restrict__ off,
                                   const int* __restrict__ idx, int tshift, int rank,
                                   long long base, unsigned char* flags) {
+  pdl_enter();
   const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= b1) return;
@@ -324,6 +340,7 @@ __global__ void k_mark_leaf_lists(long long b0, long long b1, const int* __restr
 
 __global__ void k_owner_keys(const int* __restrict__ nsel, const int* __restrict__ ids, int s0,
                              int leaf_level, unsigned* keys) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= *nsel) return;
   const int id = ids[i];
@@ -337,6 +354,7 @@ __global__ void k_leaf_pack(long long nids, const int* __restrict__ ids,
                             const int* __restrict__ leaf_off, int nmax,
                             const double2* __restrict__ pos, const double* __restrict__ g,
                             double* out) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= nids * nmax) return;
   const long long q = v / nmax;
@@ -355,6 +373,7 @@ __global__ void k_leaf_pack(long long nids, const int* __restrict__ ids,
 __global__ void k_leaf_unpack(long long nids, const int* __restrict__ ids,
                               const int* __restrict__ leaf_off, int nmax,
                               const double* __restrict__ in, double2* pos, double* g) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= nids * nmax) return;
   const long long q = v / nmax;
@@ -370,6 +389,7 @@ __global__ void k_leaf_unpack(long long nids, const int* __restrict__ ids,
 // multipole rows (p+1 complex)
 __global__ void k_row_pack(long long nids, const int* __restrict__ ids, int p,
                            const double2* __restrict__ rows, double2* out) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= nids * (p + 1)) return;
   const long long q = v / (p + 1);
@@ -379,6 +399,7 @@ __global__ void k_row_pack(long long nids, const int* __restrict__ ids, int p,
 
 __global__ void k_row_unpack(long long nids, const int* __restrict__ ids, int p,
                              const double2* __restrict__ in, double2* rows) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= nids * (p + 1)) return;
   const long long q = v / (p + 1);
@@ -389,6 +410,7 @@ __global__ void k_row_unpack(long long nids, const int* __restrict__ ids, int p,
 // level-ltop multipoles of every rank (allgather payload)
 __global__ void k_level_rows(long long k0, long long cnt, long long lbase, int p,
                              const double2* __restrict__ rows, double2* out, bool pack) {
+  pdl_enter();
   const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (v >= cnt * (p + 1)) return;
   double2* row = const_cast<double2*>(rows) + (lbase + k0) * (p + 1);
@@ -398,11 +420,13 @@ __global__ void k_level_rows(long long k0, long long cnt, long long lbase, int p
 
 __global__ void k_scatter_values(long long n, const double2* __restrict__ vals,
                                  const long long* __restrict__ idx, double2* out) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[idx[i]] = vals[i];
 }
 
 __global__ void k_fill_owned_idx(long long n, const int* __restrict__ perm, long long* out) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = perm[i];
 }
@@ -562,11 +586,11 @@ int fmm2d_dist_load(fmm2d_ctx* c, int64_t n_local, const double* d_pos, const do
     D.bbox.reserve(sizeof(unsigned long long) * 4 * 16);
     FMM_CUDA(cudaMemsetAsync(D.bbox.p, 0xff, sizeof(unsigned long long) * 4, c->st));
     note_launch();
-    k_rec_load<<<std::max(1u, std::min(nblk(n_local, 256), 1184u)), 256, 0, c->st>>>(
+    launch(k_rec_load, std::max(1u, std::min(nblk(n_local, 256), 1184u)), 256, 0, c->st, 
         n_local, reinterpret_cast<const double2*>(d_pos), d_g, idx_base, D.rec_a.as<Rec>(),
         D.bbox.as<unsigned long long>());
     note_launch();
-    k_bbox_out<<<1, 32, 0, c->st>>>(D.bbox.as<unsigned long long>(), d_bbox4);
+    launch(k_bbox_out, 1, 32, 0, c->st, D.bbox.as<unsigned long long>(), d_bbox4);
     D.seg_off = {0, n_local};
     D.d_seg_off.reserve(sizeof(long long) * 80);
     FMM_CUDA(cudaMemcpyAsync(D.d_seg_off.p, D.seg_off.data(), sizeof(long long) * 2,
@@ -601,10 +625,10 @@ int fmm2d_dist_segbox(fmm2d_ctx* c, int s, double* d_box) {
     D.bbox.reserve(sizeof(unsigned long long) * 4 * std::max(16, nseg));
     FMM_CUDA(cudaMemsetAsync(D.bbox.p, 0xff, sizeof(unsigned long long) * 4 * nseg, c->st));
     note_launch();
-    k_seg_box<<<std::max(1u, std::min(nblk(D.n_local, 256), 1184u)), 256, 0, c->st>>>(
+    launch(k_seg_box, std::max(1u, std::min(nblk(D.n_local, 256), 1184u)), 256, 0, c->st, 
         nseg, D.rec_a.as<Rec>(), D.d_seg_off.as<long long>(), D.bbox.as<unsigned long long>());
     note_launch();
-    k_keys_out<<<1, 128, 0, c->st>>>(D.bbox.as<unsigned long long>(), d_box, 4 * nseg);
+    launch(k_keys_out, 1, 128, 0, c->st, D.bbox.as<unsigned long long>(), d_box, 4 * nseg);
     return FMM2D_OK;
   });
 }
@@ -645,12 +669,12 @@ int fmm2d_dist_hist(fmm2d_ctx* c, int s, int rho, int32_t* d_hist) {
       FMM_CUDA(cudaMemcpyAsync(dk, kth.data(), sizeof(long long) * nseg, cudaMemcpyHostToDevice,
                                c->st));
       note_launch();
-      k_sel_init<<<1, 32, 0, c->st>>>(D.sel.as<SelState>(), dk, nseg);
+      launch(k_sel_init, 1, 32, 0, c->st, D.sel.as<SelState>(), dk, nseg);
       sync(c);   // ax / kth are host temporaries
     }
     FMM_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int) * 256 * nseg, c->st));
     note_launch();
-    k_sel_hist<<<std::max(1u, std::min(nblk(D.n_local, 256), 592u)), 256, 0, c->st>>>(
+    launch(k_sel_hist, std::max(1u, std::min(nblk(D.n_local, 256), 592u)), 256, 0, c->st, 
         rho, nseg, D.rec_a.as<Rec>(), D.d_seg_off.as<long long>(),
         D.d_axis.as<unsigned char>(), D.sel.as<SelState>(), d_hist);
     return FMM2D_OK;
@@ -662,7 +686,7 @@ int fmm2d_dist_pick(fmm2d_ctx* c, int s, int rho, const int32_t* d_hist) {
   return guarded(c, [&] {
     DistState& D = dist(c);
     note_launch();
-    k_sel_pick<<<1, 32, 0, c->st>>>(rho, top_segments(D, s), d_hist, D.sel.as<SelState>());
+    launch(k_sel_pick, 1, 32, 0, c->st, rho, top_segments(D, s), d_hist, D.sel.as<SelState>());
     return FMM2D_OK;
   });
 }
@@ -678,7 +702,7 @@ int fmm2d_dist_eqcount(fmm2d_ctx* c, int s, int32_t* d_eq) {
     D.eqpre.reserve(sizeof(int) * (n + 1));
     FMM_CUDA(cudaMemsetAsync(d_eq, 0, sizeof(int) * nseg, c->st));
     note_launch();
-    k_eq_count<<<std::max(1u, std::min(nblk(D.n_local, 256), 1184u)), 256, 0, c->st>>>(
+    launch(k_eq_count, std::max(1u, std::min(nblk(D.n_local, 256), 1184u)), 256, 0, c->st, 
         nseg, D.rec_a.as<Rec>(), D.d_seg_off.as<long long>(), D.d_axis.as<unsigned char>(),
         D.sel.as<SelState>(), d_eq, D.eqf.as<int>());
     return FMM2D_OK;
@@ -704,7 +728,7 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
       for (DBuf* b : {&D.skey, &D.skey2}) b->reserve(sizeof(unsigned) * n);
       for (DBuf* b : {&D.sval, &D.sval2}) b->reserve(sizeof(int) * n);
       note_launch();
-      k_side_keys<<<std::min(nblk(n, 256), 1184u), 256, 0, c->st>>>(
+      launch(k_side_keys, std::min(nblk(n, 256), 1184u), 256, 0, c->st, 
           nseg, D.part.G, D.part.rank, D.rec_a.as<Rec>(), D.d_seg_off.as<long long>(),
           D.d_axis.as<unsigned char>(), D.sel.as<SelState>(), d_eq_all, D.eqpre.as<int>(),
           D.skey.as<unsigned>(), D.sval.as<int>());
@@ -712,12 +736,12 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
                  D.sval2.as<int>(), n, s + 1, c->st);
       D.rec_b.reserve(sizeof(Rec) * n);
       note_launch();
-      k_rec_gather<<<nblk(n, 256), 256, 0, c->st>>>(n, D.sval2.as<int>(), D.rec_a.as<Rec>(),
+      launch(k_rec_gather, nblk(n, 256), 256, 0, c->st, n, D.sval2.as<int>(), D.rec_a.as<Rec>(),
                                                     D.rec_b.as<Rec>());
       D.rec_a.swap(D.rec_b);
     }
     note_launch();
-    k_seg_bounds<<<nblk(n + 1, 256), 256, 0, c->st>>>(n, 2 * nseg, D.skey2.as<unsigned>(),
+    launch(k_seg_bounds, nblk(n + 1, 256), 256, 0, c->st, n, 2 * nseg, D.skey2.as<unsigned>(),
                                                       D.d_seg_off.as<long long>());
     // cut values and child rectangles (tree.py:281-285)
     std::vector<SelState> sel(nseg);
@@ -773,7 +797,7 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
     D.loc_g.reserve(sizeof(double) * n);
     D.loc_idx.reserve(sizeof(int) * n);
     note_launch();
-    k_rec_unpack<<<nblk(n, 256), 256, 0, c->st>>>(n, reinterpret_cast<const Rec*>(d_recv),
+    launch(k_rec_unpack, nblk(n, 256), 256, 0, c->st, n, reinterpret_cast<const Rec*>(d_recv),
                                                   D.loc_pos.as<double2>(), D.loc_g.as<double>(),
                                                   D.loc_idx.as<int>());
     TreeState& T = c->T;
@@ -854,7 +878,7 @@ int fmm2d_dist_geom_pack(fmm2d_ctx* c, double* d_send) {
     const TreeState& T = c->T;
     const long long cnt = own_count(D);
     note_launch();
-    k_geo_pack<<<nblk(cnt, 256), 256, 0, c->st>>>(cnt, D.part.ltop(), D.part.s0, D.part.rank,
+    launch(k_geo_pack, nblk(cnt, 256), 256, 0, c->st, cnt, D.part.ltop(), D.part.s0, D.part.rank,
                                                   T.box_cx.as<double>(), T.box_cy.as<double>(),
                                                   T.box_hw.as<double>(), T.box_hh.as<double>(),
                                                   T.box_r.as<double>(), d_send);
@@ -874,7 +898,7 @@ int fmm2d_dist_connect(fmm2d_ctx* c, const double* d_geo_all, int64_t* req_count
     const int G = D.part.G, s0 = D.part.s0, rank = D.part.rank, L = D.L;
     const long long cnt = own_count(D);
     note_launch();
-    k_geo_unpack<<<nblk(cnt * G, 256), 256, 0, c->st>>>(
+    launch(k_geo_unpack, nblk(cnt * G, 256), 256, 0, c->st, 
         cnt, G, D.part.ltop(), s0, d_geo_all, T.box_cx.as<double>(), T.box_cy.as<double>(),
         T.box_hw.as<double>(), T.box_hh.as<double>(), T.box_r.as<double>());
     record(c, 2);
@@ -897,16 +921,16 @@ int fmm2d_dist_connect(fmm2d_ctx* c, const double* d_geo_all, int64_t* req_count
     const long long b0 = D.part.lo(L), b1 = D.part.hi(L);
     const int tshift = 2 * L - s0;
     note_launch();
-    k_mark_weak<<<1184, 256, 0, c->st>>>(Ls.weak_off.as<int>() + nbox, Ls.weak_idx.as<int>(), s0,
+    launch(k_mark_weak, 1184, 256, 0, c->st, Ls.weak_off.as<int>() + nbox, Ls.weak_idx.as<int>(), s0,
                                          rank, fb);
     note_launch();
-    k_mark_leaf_lists<<<nblk((b1 - b0) * 32, 256), 256, 0, c->st>>>(
+    launch(k_mark_leaf_lists, nblk((b1 - b0) * 32, 256), 256, 0, c->st, 
         b0, b1, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), tshift, rank, level_base(L), fb);
     note_launch();
-    k_mark_leaf_lists<<<nblk((b1 - b0) * 32, 256), 256, 0, c->st>>>(
+    launch(k_mark_leaf_lists, nblk((b1 - b0) * 32, 256), 256, 0, c->st, 
         b0, b1, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), tshift, rank, 0, fl);
     note_launch();
-    k_mark_leaf_lists<<<nblk((b1 - b0) * 32, 256), 256, 0, c->st>>>(
+    launch(k_mark_leaf_lists, nblk((b1 - b0) * 32, 256), 256, 0, c->st, 
         b0, b1, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), tshift, rank, 0, fl);
     for (int kind = 0; kind < 2; ++kind) {
       const long long nn = kind == 0 ? nbox : nleaf;
@@ -929,7 +953,7 @@ int fmm2d_dist_connect(fmm2d_ctx* c, const double* d_geo_all, int64_t* req_count
       std::vector<unsigned> keys(nsel);
       if (nsel > 0) {
         note_launch();
-        k_owner_keys<<<nblk(nsel, 256), 256, 0, c->st>>>(D.nsel.as<int>(), D.ids.as<int>(), s0,
+        launch(k_owner_keys, nblk(nsel, 256), 256, 0, c->st, D.nsel.as<int>(), D.ids.as<int>(), s0,
                                                          kind == 0 ? -1 : L,
                                                          D.keys.as<unsigned>());
         int bits = 1;
@@ -979,11 +1003,11 @@ int fmm2d_dist_pack(fmm2d_ctx* c, int kind, const int32_t* d_ids, int64_t nids, 
     const TreeState& T = c->T;
     note_launch();
     if (kind == 1)
-      k_leaf_pack<<<nblk(nids * D.nmax_leaf, 256), 256, 0, c->st>>>(
+      launch(k_leaf_pack, nblk(nids * D.nmax_leaf, 256), 256, 0, c->st, 
           nids, d_ids, D.leaf_off.as<int>(), (int)D.nmax_leaf, T.src_pos.as<double2>(),
           T.src_g.as<double>(), d_send);
     else
-      k_row_pack<<<nblk(nids * (D.p + 1), 256), 256, 0, c->st>>>(
+      launch(k_row_pack, nblk(nids * (D.p + 1), 256), 256, 0, c->st, 
           nids, d_ids, D.p, c->E.mult.as<double2>() + 0, reinterpret_cast<double2*>(d_send));
     return FMM2D_OK;
   });
@@ -999,11 +1023,11 @@ int fmm2d_dist_unpack(fmm2d_ctx* c, int kind, const double* d_recv) {
     TreeState& T = c->T;
     note_launch();
     if (kind == 1)
-      k_leaf_unpack<<<nblk(nids * D.nmax_leaf, 256), 256, 0, c->st>>>(
+      launch(k_leaf_unpack, nblk(nids * D.nmax_leaf, 256), 256, 0, c->st, 
           nids, D.req_ids[1].as<int>(), D.leaf_off.as<int>(), (int)D.nmax_leaf, d_recv,
           T.src_pos.as<double2>(), T.src_g.as<double>());
     else
-      k_row_unpack<<<nblk(nids * (D.p + 1), 256), 256, 0, c->st>>>(
+      launch(k_row_unpack, nblk(nids * (D.p + 1), 256), 256, 0, c->st, 
           nids, D.req_ids[0].as<int>(), D.p, reinterpret_cast<const double2*>(d_recv),
           c->E.mult.as<double2>());
     return FMM2D_OK;
@@ -1026,7 +1050,7 @@ int fmm2d_dist_upward(fmm2d_ctx* c, double* d_top_send, int64_t* top_boxes) {
     run_m2m(T, E, c->st, D.part, std::max(lt, 1), L - 1);
     const long long k0 = D.part.lo(lt), cnt = D.part.hi(lt) - k0;
     note_launch();
-    k_level_rows<<<nblk(cnt * (p + 1), 256), 256, 0, c->st>>>(
+    launch(k_level_rows, nblk(cnt * (p + 1), 256), 256, 0, c->st, 
         k0, cnt, level_base(lt), p, E.mult.as<double2>(), reinterpret_cast<double2*>(d_top_send),
         true);
     *top_boxes = cnt;
@@ -1044,7 +1068,7 @@ int fmm2d_dist_upward_top(fmm2d_ctx* c, const double* d_top_all) {
     const int p = D.p, lt = D.part.ltop();
     const long long nb = 1ll << (2 * lt);
     note_launch();
-    k_level_rows<<<nblk(nb * (p + 1), 256), 256, 0, c->st>>>(
+    launch(k_level_rows, nblk(nb * (p + 1), 256), 256, 0, c->st, 
         0, nb, level_base(lt), p, E.mult.as<double2>(),
         const_cast<double2*>(reinterpret_cast<const double2*>(d_top_all)), false);
     if (lt - 1 >= 1) run_m2m(T, E, c->st, D.part, 1, lt - 1);
@@ -1075,7 +1099,7 @@ int fmm2d_dist_downward(fmm2d_ctx* c, double* d_vals, int64_t* d_idx, fmm2d_repo
     run_p2p(T, Ls, E, D.leaf_off.as<int>(), reinterpret_cast<double2*>(d_vals), dst, c->st,
             D.part, D.g0);
     note_launch();
-    k_fill_owned_idx<<<nblk(D.n_r, 256), 256, 0, c->st>>>(
+    launch(k_fill_owned_idx, nblk(D.n_r, 256), 256, 0, c->st, 
         D.n_r, T.src_perm.as<int>() + D.g0, reinterpret_cast<long long*>(d_idx));
     record(c, 11);
     run_stats(T, Ls, dst, c->st, D.part);
@@ -1137,7 +1161,7 @@ int fmm2d_scatter_values(fmm2d_ctx* c, int64_t n, const double* d_vals, const in
   return guarded(c, [&] {
     if (n <= 0) return FMM2D_OK;
     note_launch();
-    k_scatter_values<<<nblk(n, 256), 256, 0, c->st>>>(
+    launch(k_scatter_values, nblk(n, 256), 256, 0, c->st, 
         n, reinterpret_cast<const double2*>(d_vals), reinterpret_cast<const long long*>(d_idx),
         reinterpret_cast<double2*>(d_out));
     return FMM2D_OK;

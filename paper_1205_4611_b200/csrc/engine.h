@@ -156,6 +156,23 @@ struct ExpState {
 extern long long g_launches;
 inline void note_launch() { ++g_launches; }
 
+// launch an engine kernel with programmatic dependent launch (see pdl_enter)
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FMM_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // ---------------------------------------------------------------------------
 // launchers (all enqueue on `st`, no host sync)
 int plan_levels(int64_t n, int nd);

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(128)
 k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double* __restrict__ cx, const double* __restrict__ cy, double2* mult, int p) {
+  pdl_enter();
   const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (b >= b1) return;
   const long long gb = level_base(L) + b;
@@ -106,6 +107,7 @@ k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
            const double2* __restrict__ src_pos, const double* __restrict__ src_g,
            const double* __restrict__ cx, const double* __restrict__ cy, double2* rows, int p,
            DevStatus* st) {
+  pdl_enter();
   if (lists_overflowed(st)) return;
   const long long lb = level_base(L);
   const int qbase = l_off[b0], qend = l_off[b1];
@@ -147,6 +149,7 @@ k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
 __global__ void __launch_bounds__(128)
 k_p2l_fold(int L, long long b0, long long b1, const int* __restrict__ l_off,
            const double2* __restrict__ rows, double2* local, int p, DevStatus* st) {
+  pdl_enter();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long b = b0 + t / (p + 1);
   const int j = (int)(t % (p + 1));
@@ -198,6 +201,7 @@ template <int PM>
 __global__ void __launch_bounds__(128)
 k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* mult, int p) {
+  pdl_enter();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long k = k0 + (t >> 2);
   const int c = (int)(t & 3), lane = threadIdx.x & 31;
@@ -228,6 +232,7 @@ template <int PM>
 __global__ void __launch_bounds__(128)
 k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* local, int p) {
+  pdl_enter();
   // parent level l, child level l+1 (children [c0, c1))
   const long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (c >= c1) return;
@@ -363,6 +368,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
             const int* __restrict__ w_tgt, const double* __restrict__ cx,
             const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
             double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+  pdl_enter();
   static_assert(2 * PM <= PASCAL_N, "Pascal table too small for this order");
   using Cfg = M2LDenseCfg<PM>;
   if (lists_overflowed(st)) return;
@@ -479,6 +485,7 @@ __global__ void __launch_bounds__(128)
 k_m2l_target(long long nbox, const int* __restrict__ woff, const int* __restrict__ w_src,
              const double* __restrict__ cx, const double* __restrict__ cy,
              const double2* __restrict__ mult, double2* local, int p, DevStatus* st) {
+  pdl_enter();
   if (lists_overflowed(st)) return;
   const int lane = threadIdx.x & 31, h = lane & 1, pl = lane >> 1;
   const unsigned long long hm = h ? ~0ull : 0ull;
@@ -559,6 +566,7 @@ __global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __rest
                             const double2* __restrict__ partials,
                             const unsigned char* __restrict__ item_flags, double2* local, int p,
                             int item_pairs, const DevStatus* st) {
+  pdl_enter();
   if (lists_overflowed(st)) return;
   const long long npairs = *total_ptr;
   const long long nitems = (npairs + item_pairs - 1) / item_pairs;
@@ -597,6 +605,7 @@ k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __rest
           const int* __restrict__ m_idx, const double* __restrict__ cx,
           const double* __restrict__ cy, const double2* __restrict__ mult,
           const double2* __restrict__ local, double2* phi, int p, DevStatus* st) {
+  pdl_enter();
   // evaluation points [e0, e1) of m (tree order)
   const long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= e1 || lists_overflowed(st)) return;
@@ -642,6 +651,7 @@ constexpr int M2P_LONG_POINTS = 8;      // points per pass (SMEM: 8 x 256 comple
 
 __global__ void k_m2p_find_long(long long b0, long long b1, const int* __restrict__ m_off,
                                 int* list, int* count) {
+  pdl_enter();
   const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (b < b1 && m_off[b + 1] - m_off[b] > M2P_INLINE) list[atomicAdd(count, 1)] = (int)b;
 }
@@ -653,6 +663,7 @@ k_m2p_long(int L, const int* __restrict__ list, const int* __restrict__ count,
            const int* __restrict__ m_off, const int* __restrict__ m_idx,
            const double* __restrict__ cx, const double* __restrict__ cy,
            const double2* __restrict__ mult, double2* phi, int p, DevStatus* st) {
+  pdl_enter();
   __shared__ double2 red[M2P_LONG_POINTS][M2P_LONG_THREADS];
   if (lists_overflowed(st)) return;
   const int n = *count;
@@ -726,17 +737,17 @@ struct Launch {
     if (L == 0) return;
     const long long b0 = part.lo(L), b1 = part.hi(L);
     note_launch();
-    k_p2m<PM><<<nblk(b1 - b0, 128), 128, 0, st>>>(L, b0, b1, offL, T.src_pos.as<double2>(),
+    launch(k_p2m<PM>, nblk(b1 - b0, 128), 128, 0, st, L, b0, b1, offL, T.src_pos.as<double2>(),
                                                   T.src_g.as<double>(), T.box_cx.as<double>(),
                                                   T.box_cy.as<double>(), E.mult.as<double2>(), p);
     note_launch();
     E.p2l_rows.reserve(sizeof(double2) * std::max(1ll, Ls.cap_p2l) * (p + 1));
-    k_p2l_pair<PM><<<8 * sm_count(), 128, 0, st>>>(
+    launch(k_p2l_pair<PM>, 8 * sm_count(), 128, 0, st, 
         L, b0, b1, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.p2l_rows.as<double2>(), p, dstat);
     note_launch();
-    k_p2l_fold<<<nblk((b1 - b0) * (p + 1), 128), 128, 0, st>>>(
+    launch(k_p2l_fold, nblk((b1 - b0) * (p + 1), 128), 128, 0, st, 
         L, b0, b1, Ls.p2l_off.as<int>(), E.p2l_rows.as<double2>(), E.local.as<double2>(), p,
         dstat);
   }
@@ -745,7 +756,7 @@ struct Launch {
     for (int l = lmax; l >= lmin; --l) {
       const long long k0 = part.lo(l), k1 = part.hi(l);
       note_launch();
-      k_m2m<PM><<<nblk(4 * (k1 - k0), 128), 128, 0, st>>>(l, k0, k1, T.box_cx.as<double>(),
+      launch(k_m2m<PM>, nblk(4 * (k1 - k0), 128), 128, 0, st, l, k0, k1, T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), E.mult.as<double2>(),
                                                     E.p);
     }
@@ -776,12 +787,12 @@ struct Launch {
       const unsigned grid = (unsigned)std::min<long long>(std::max(1ll, items),
                                                           (long long)Cfg::MINB * sm_count());
       note_launch();
-      k_m2l_dense<PM><<<grid, M2L_ITEM, Cfg::SMEM, st>>>(
+      launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st, 
           total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
           T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
           E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
       note_launch();
-      k_m2l_fixup<<<std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st>>>(
+      launch(k_m2l_fixup, std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st, 
           total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
           E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, M2L_ITEM, dstat);
     }
@@ -791,7 +802,7 @@ struct Launch {
     const long long nbox = level_base(T.L + 1);
     const unsigned grid = (unsigned)std::min<long long>(nblk(nbox * 32, 128), 64ll * sm_count());
     note_launch();
-    k_m2l_target<PM><<<grid, 128, 0, st>>>(nbox, Ls.weak_off.as<int>(), Ls.weak_idx.as<int>(),
+    launch(k_m2l_target<PM>, grid, 128, 0, st, nbox, Ls.weak_off.as<int>(), Ls.weak_idx.as<int>(),
                                            T.box_cx.as<double>(), T.box_cy.as<double>(),
                                            E.mult.as<double2>(), E.local.as<double2>(), E.p,
                                            dstat);
@@ -800,7 +811,7 @@ struct Launch {
     for (int l = 1; l < T.L; ++l) {
       const long long c0 = part.lo(l + 1), c1 = part.hi(l + 1);
       note_launch();
-      k_l2l<PM><<<nblk(c1 - c0, 128), 128, 0, st>>>(l, c0, c1, T.box_cx.as<double>(),
+      launch(k_l2l<PM>, nblk(c1 - c0, 128), 128, 0, st, l, c0, c1, T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), E.local.as<double2>(),
                                                     E.p);
     }
@@ -858,7 +869,7 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
   if (e1 <= e0) return;
   dispatch_p(E.p, [&](auto pm) {
     note_launch();
-    k_l2p_m2p<decltype(pm)::value><<<nblk(e1 - e0, 128), 128, 0, st>>>(
+    launch(k_l2p_m2p<decltype(pm)::value>, nblk(e1 - e0, 128), 128, 0, st, 
         T.m, e0, e1, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
         T.box_cx.as<double>(), T.box_cy.as<double>(), E.mult.as<double2>(),
         E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
@@ -873,10 +884,10 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
     int* cnt = E.long_list.as<int>() + nleaf;
     FMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), st));
     note_launch();
-    k_m2p_find_long<<<nblk(b1 - b0, 256), 256, 0, st>>>(b0, b1, Ls.m2p_off.as<int>(),
+    launch(k_m2p_find_long, nblk(b1 - b0, 256), 256, 0, st, b0, b1, Ls.m2p_off.as<int>(),
                                                         E.long_list.as<int>(), cnt);
     note_launch();
-    k_m2p_long<decltype(pm)::value><<<2 * 148, M2P_LONG_THREADS, 0, st>>>(
+    launch(k_m2p_long<decltype(pm)::value>, 2 * 148, M2P_LONG_THREADS, 0, st, 
         T.L, E.long_list.as<int>(), cnt, T.eoff_t, T.epos_t, Ls.m2p_off.as<int>(),
         Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.mult.as<double2>(), E.phi.as<double2>(), E.p, dstat);

@@ -77,6 +77,7 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double2* __restrict__ eval_pos, const int* __restrict__ eval_perm,
       const double2* __restrict__ phi_in, double2* values, long long out_base, DevStatus* st) {
+  pdl_enter();
   __shared__ double2 s_pos[P2P_WARPS][P2P_CHUNK];
   __shared__ double s_g[P2P_WARPS][P2P_CHUNK];
   const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
@@ -177,6 +178,7 @@ constexpr int DIRECT_TILE = 256;
 __global__ void __launch_bounds__(DIRECT_TILE)
 k_direct(const double2* __restrict__ src, const double* __restrict__ g, long long n,
          const double2* __restrict__ tgt, long long m, double2* out) {
+  pdl_enter();
   __shared__ double sx[DIRECT_TILE], sy[DIRECT_TILE], sg[DIRECT_TILE];
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const double2 y = t < m ? tgt[t] : make_double2(0.0, 0.0);
@@ -214,7 +216,7 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
              long long out_base) {
   const long long b0 = part.lo(T.L), b1 = part.hi(T.L);
   note_launch();
-  k_p2p<<<nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0, st>>>(
+  launch(k_p2p, nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0, st, 
       b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), T.src_pos.as<double2>(),
       T.src_g.as<double>(), T.epos_t, out_base >= 0 ? nullptr : T.eperm_t, E.phi.as<double2>(),
       values, out_base, dstat);
@@ -223,7 +225,7 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
                 double2* out, cudaStream_t st) {
   note_launch();
-  k_direct<<<nblk(m, DIRECT_TILE), DIRECT_TILE, 0, st>>>(src, g, n, tgt, m, out);
+  launch(k_direct, nblk(m, DIRECT_TILE), DIRECT_TILE, 0, st, src, g, n, tgt, m, out);
 }
 
 }  // namespace fmm

@@ -17,6 +17,7 @@ constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
 __global__ void __launch_bounds__(SCAN_THREADS)
 scan_tiles(const int* __restrict__ in, int* __restrict__ out, long long n,
            unsigned long long* status, unsigned int* counter, const int* base_ptr) {
+  pdl_enter();
   __shared__ unsigned int s_tile;
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ long long s_excl;
@@ -87,6 +88,7 @@ scan_tiles(const int* __restrict__ in, int* __restrict__ out, long long n,
 }
 
 __global__ void write_base_total(int* out, const int* base_ptr) {
+  pdl_enter();
   out[0] = base_ptr ? *base_ptr : 0;
 }
 
@@ -96,7 +98,7 @@ void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t 
                     const int* base) {
   if (n <= 0) {
     note_launch();
-    write_base_total<<<1, 1, 0, st>>>(out, base);
+    launch(write_base_total, 1, 1, 0, st, out, base);
     return;
   }
   const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -106,7 +108,7 @@ void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t 
   auto* status = tmp.as<unsigned long long>();
   auto* counter = reinterpret_cast<unsigned int*>(status + tiles);
   note_launch();
-  scan_tiles<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, status, counter, base);
+  launch(scan_tiles, (unsigned)tiles, SCAN_THREADS, 0, st, in, out, n, status, counter, base);
 }
 
 }  // namespace fmm

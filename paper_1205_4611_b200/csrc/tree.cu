@@ -78,6 +78,7 @@ __device__ __forceinline__ void block_minmax(double& x0, double& x1, double& y0,
 __global__ void __launch_bounds__(256)
 k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__ epos,
        long long m, Rect* root, unsigned int* counter, double* partial) {
+  pdl_enter();
   double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n + m;
        i += (long long)gridDim.x * blockDim.x) {
@@ -113,6 +114,7 @@ k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__
 // rank keys
 __global__ void k_make_keys(const double2* __restrict__ pos, long long n, int axis,
                             unsigned long long* keys, int* vals) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double2 z = pos[i];
@@ -126,6 +128,7 @@ __global__ void k_make_keys(const double2* __restrict__ pos, long long n, int ax
 // k_fix_ties then orders exactly by (coordinate, index).
 __global__ void k_make_keys32(const double2* __restrict__ pos, long long n, int axis,
                               const Rect* __restrict__ root, unsigned* keys, int* vals) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Rect r = *root;
@@ -149,6 +152,7 @@ constexpr int TIE_RUN_MAX = 64;
 __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
                            const double2* __restrict__ pos, int axis, long long n,
                            DevStatus* st) {
+  pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned k = keys[i];
@@ -186,6 +190,7 @@ __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
 // inverse permutation: rank of every point along the sorted axis (an
 // L2-resident scatter; the coordinates are looked up only at the cuts)
 __global__ void k_rank_scatter(long long n, const int* __restrict__ perm, int* rank) {
+  pdl_enter();
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (r < n) rank[perm[r]] = (int)r;
 }
@@ -194,6 +199,7 @@ __global__ void k_init_arrays(long long n, const int* __restrict__ perm_x,
                               const int* __restrict__ perm_y, const int* __restrict__ rank_x,
                               const int* __restrict__ rank_y, int2* X, int2* Y,
                               unsigned char* xpar, unsigned char* ypar) {
+  pdl_enter();
   long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (r == 0) { xpar[0] = 0; ypar[0] = 0; }
   if (r >= n) return;
@@ -271,6 +277,7 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
             const int* __restrict__ tile_start, int2* X0, int2* X1, int2* Y0, int2* Y1,
             const unsigned char* xpar, const unsigned char* ypar, unsigned char* xpar_next,
             unsigned char* ypar_next, LookbackPacked lbs, unsigned ntiles, DevStatus* st) {
+  pdl_enter();
   __shared__ unsigned s_tile;
   __shared__ int sw[PART_THREADS / 32];
   __shared__ long long s_excl;
@@ -369,6 +376,7 @@ struct SubArgs {
 
 __global__ void __launch_bounds__(SUB_THREADS)
 k_subtree(SubArgs A, DevStatus* st) {
+  pdl_enter();
   extern __shared__ unsigned char smem_raw[];
   const long long j0 = blockIdx.x;
   const int* off_sb = A.a.off + off_base(A.sb);
@@ -517,6 +525,7 @@ k_subtree(SubArgs A, DevStatus* st) {
 __global__ void k_global_leaf_of(int S, const int* __restrict__ offS, const int2* X0,
                                  const int2* X1, const unsigned char* __restrict__ xpar,
                                  const int* __restrict__ perm_x, long long n, int* leaf_of) {
+  pdl_enter();
   // used when every split ran globally: leaf = segment of the final step
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -530,6 +539,7 @@ __global__ void k_global_leaf_of(int S, const int* __restrict__ offS, const int2
 }
 
 __global__ void k_iota_perm(int* v, long long n) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) v[i] = (int)i;
 }
@@ -538,6 +548,7 @@ __global__ void k_descend(const double2* __restrict__ pts, long long m, int S,
                           const double* __restrict__ cut_tab,
                           const unsigned char* __restrict__ axis_tab, unsigned int* keys,
                           int* vals) {
+  pdl_enter();
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= m) return;
   const double2 z = pts[e];
@@ -553,6 +564,7 @@ __global__ void k_descend(const double2* __restrict__ pts, long long m, int S,
 
 __global__ void k_iota_keys(const int* __restrict__ leaf_of, long long n, unsigned int* keys,
                             int* vals) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   keys[i] = (unsigned int)leaf_of[i];
@@ -562,7 +574,8 @@ __global__ void k_iota_keys(const int* __restrict__ leaf_of, long long n, unsign
 __global__ void k_gather_points(const int* __restrict__ perm, long long m,
                                 const double2* __restrict__ pts, const double* __restrict__ g,
                                 double2* out_pos, double* out_g, int* out_perm,
-                                long long out0 = 0, const int* __restrict__ orig = nullptr) {
+                                long long out0, const int* __restrict__ orig) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= m) return;
   int e = perm[i];
@@ -574,6 +587,7 @@ __global__ void k_gather_points(const int* __restrict__ perm, long long m,
 // leaf offsets from leaf-sorted keys (handles empty leaves)
 __global__ void k_leaf_offsets(const unsigned int* __restrict__ skeys, long long m, long long nleaf,
                                int* leaf_off) {
+  pdl_enter();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > m) return;
   long long prev = i == 0 ? -1 : (long long)skeys[i - 1];
@@ -582,6 +596,7 @@ __global__ void k_leaf_offsets(const unsigned int* __restrict__ skeys, long long
 }
 
 __global__ void k_leaf_offsets_identity(int* leaf_off, long long m) {
+  pdl_enter();
   leaf_off[0] = 0;
   leaf_off[1] = (int)m;
 }
@@ -589,6 +604,7 @@ __global__ void k_leaf_offsets_identity(int* leaf_off, long long m) {
 // per-level box geometry from the rectangles of even steps (tree.py:375-377)
 __global__ void k_level_geometry(int L, const Rect* __restrict__ rect_tab, double* cx, double* cy,
                                  double* hw, double* hh, double* r, int s0, long long seg) {
+  pdl_enter();
   long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = level_base(L + 1);
   if (gid >= total) return;
@@ -739,7 +755,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     FMM_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
     unsigned blocks = (unsigned)std::min<long long>(1024, std::max<long long>(1, nblk(n + m, 256)));
     note_launch();
-    k_bbox<<<blocks, 256, 0, st>>>(pos, n, epos, T.aliased ? 0 : m, T.rect_tab.as<Rect>(),
+    launch(k_bbox, blocks, 256, 0, st, pos, n, epos, T.aliased ? 0 : m, T.rect_tab.as<Rect>(),
                                    counter, bb + 4);
   }
 
@@ -752,26 +768,26 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         auto* kin = T.keys_in.as<unsigned long long>();
         auto* kout = T.keys_out.as<unsigned long long>();
         note_launch();
-        k_make_keys<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, kin, T.vals_in.as<int>());
+        launch(k_make_keys, nblk(n, 256), 256, 0, st, pos, n, axis, kin, T.vals_in.as<int>());
         radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 64, st);
       } else {
         auto* kin = reinterpret_cast<unsigned*>(T.keys_in.p);
         auto* kout = reinterpret_cast<unsigned*>(T.keys_out.p);
         note_launch();
-        k_make_keys32<<<nblk(n, 256), 256, 0, st>>>(pos, n, axis, T.rect_tab.as<Rect>(), kin,
+        launch(k_make_keys32, nblk(n, 256), 256, 0, st, pos, n, axis, T.rect_tab.as<Rect>(), kin,
                                                     T.vals_in.as<int>());
         radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 32, st);
         note_launch();
-        k_fix_ties<<<nblk(n, 256), 256, 0, st>>>(kout, perm, pos, axis, n, dstat);
+        launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, dstat);
       }
       note_launch();
-      k_rank_scatter<<<nblk(n, 256), 256, 0, st>>>(n, perm, axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
+      launch(k_rank_scatter, nblk(n, 256), 256, 0, st, n, perm, axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
     }
     for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
     const long long pmax = (1ll << std::max(sb, 1)) + 2;
     for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
     note_launch();
-    k_init_arrays<<<nblk(n, 256), 256, 0, st>>>(n, T.perm_x.as<int>(), T.perm_y.as<int>(),
+    launch(k_init_arrays, nblk(n, 256), 256, 0, st, n, T.perm_x.as<int>(), T.perm_y.as<int>(),
                                                 T.rank_x.as<int>(), T.rank_y.as<int>(),
                                                 T.X0.as<int2>(), T.Y0.as<int2>(),
                                                 T.xpar0.as<unsigned char>(),
@@ -802,7 +818,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       const LookbackPacked lbs{T.lb_vals.as<unsigned long long>(), T.lb_ticket.as<unsigned>(),
                                T.lb_epoch};
       note_launch();
-      k_part_step<<<nt, PART_THREADS, 0, st>>>(a, s, tseg, tstart, T.X0.as<int2>(),
+      launch(k_part_step, nt, PART_THREADS, 0, st, a, s, tseg, tstart, T.X0.as<int2>(),
                                                T.X1.as<int2>(), T.Y0.as<int2>(), T.Y1.as<int2>(),
                                                xp, yp, xq, yq, lbs, (unsigned)nt, dstat);
       std::swap(xp, xq);
@@ -817,10 +833,10 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       FMM_CUDA(cudaFuncSetAttribute(k_subtree, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     P.smem_bytes));
       note_launch();
-      k_subtree<<<(unsigned)(1ll << sb), SUB_THREADS, P.smem_bytes, st>>>(A, dstat);
+      launch(k_subtree, (unsigned)(1ll << sb), SUB_THREADS, P.smem_bytes, st, A, dstat);
       if (!P.global_leaf_finalize) {
         note_launch();
-        k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.leaf_of.as<int>(), n, pos, T.g_p,
+        launch(k_gather_points, nblk(n, 256), 256, 0, st, T.leaf_of.as<int>(), n, pos, T.g_p,
                                                       T.src_pos.as<double2>(),
                                                       T.src_g.as<double>(),
                                                       T.src_perm.as<int>(), spec.out0,
@@ -829,7 +845,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     } else {
       // every split ran as a global step: leaves are segments of the global copies
       note_launch();
-      k_global_leaf_of<<<nblk(n, 256), 256, 0, st>>>(S, P.d_off.as<int>() + off_base(S), X0, X1,
+      launch(k_global_leaf_of, nblk(n, 256), 256, 0, st, S, P.d_off.as<int>() + off_base(S), X0, X1,
                                                      xp, T.perm_x.as<int>(), n,
                                                      T.leaf_of.as<int>());
     }
@@ -837,10 +853,10 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
       auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
       note_launch();
-      k_iota_keys<<<nblk(n, 256), 256, 0, st>>>(T.leaf_of.as<int>(), n, kin, T.vals_in.as<int>());
+      launch(k_iota_keys, nblk(n, 256), 256, 0, st, T.leaf_of.as<int>(), n, kin, T.vals_in.as<int>());
       radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), n, S, st);
       note_launch();
-      k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_out.as<int>(), n, pos, T.g_p,
+      launch(k_gather_points, nblk(n, 256), 256, 0, st, T.vals_out.as<int>(), n, pos, T.g_p,
                                                     T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                     T.src_perm.as<int>(), spec.out0, spec.orig);
     }
@@ -855,16 +871,16 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       auto* kin = reinterpret_cast<unsigned int*>(T.keys_in.p);
       auto* kout = reinterpret_cast<unsigned int*>(T.keys_out.p);
       note_launch();
-      k_descend<<<nblk(m, 256), 256, 0, st>>>(epos, m, S, T.cut_tab.as<double>(),
+      launch(k_descend, nblk(m, 256), 256, 0, st, epos, m, S, T.cut_tab.as<double>(),
                                               T.axis_tab.as<unsigned char>(), kin,
                                               T.vals_in.as<int>());
       radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), T.vals_out.as<int>(), m, S, st);
       note_launch();
-      k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_out.as<int>(), m, epos, nullptr,
+      launch(k_gather_points, nblk(m, 256), 256, 0, st, T.vals_out.as<int>(), m, epos, nullptr,
                                                     T.eval_pos.as<double2>(), nullptr,
-                                                    T.eval_perm.as<int>());
+                                                    T.eval_perm.as<int>(), 0ll, nullptr);
       note_launch();
-      k_leaf_offsets<<<nblk(m + 1, 256), 256, 0, st>>>(kout, m, 1ll << S, T.eval_leaf_off.as<int>());
+      launch(k_leaf_offsets, nblk(m + 1, 256), 256, 0, st, kout, m, 1ll << S, T.eval_leaf_off.as<int>());
       T.epos_t = T.eval_pos.as<double2>();
       T.eperm_t = T.eval_perm.as<int>();
       T.eoff_t = T.eval_leaf_off.as<int>();
@@ -873,9 +889,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   } else {
     // L == 0: a single box, identity permutations (tree.py:316-317)
     note_launch();
-    k_iota_perm<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n);
+    launch(k_iota_perm, nblk(n, 256), 256, 0, st, T.vals_in.as<int>(), n);
     note_launch();
-    k_gather_points<<<nblk(n, 256), 256, 0, st>>>(T.vals_in.as<int>(), n, pos, T.g_p,
+    launch(k_gather_points, nblk(n, 256), 256, 0, st, T.vals_in.as<int>(), n, pos, T.g_p,
                                                   T.src_pos.as<double2>(), T.src_g.as<double>(),
                                                   T.src_perm.as<int>(), spec.out0, spec.orig);
     if (T.aliased) {
@@ -883,20 +899,20 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       T.eperm_t = T.src_perm.as<int>();
     } else {
       note_launch();
-      k_iota_perm<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m);
+      launch(k_iota_perm, nblk(m, 256), 256, 0, st, T.vals_in.as<int>(), m);
       note_launch();
-      k_gather_points<<<nblk(m, 256), 256, 0, st>>>(T.vals_in.as<int>(), m, epos, nullptr,
+      launch(k_gather_points, nblk(m, 256), 256, 0, st, T.vals_in.as<int>(), m, epos, nullptr,
                                                     T.eval_pos.as<double2>(), nullptr,
-                                                    T.eval_perm.as<int>());
+                                                    T.eval_perm.as<int>(), 0ll, nullptr);
       T.epos_t = T.eval_pos.as<double2>();
       T.eperm_t = T.eval_perm.as<int>();
     }
     note_launch();
-    k_leaf_offsets_identity<<<1, 1, 0, st>>>(T.eval_leaf_off.as<int>(), m);
+    launch(k_leaf_offsets_identity, 1, 1, 0, st, T.eval_leaf_off.as<int>(), m);
     T.eoff_t = T.eval_leaf_off.as<int>();
   }
   note_launch();
-  k_level_geometry<<<nblk(nbox, 256), 256, 0, st>>>(L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
+  launch(k_level_geometry, nblk(nbox, 256), 256, 0, st, L, T.rect_tab.as<Rect>(), T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), T.box_hw.as<double>(),
                                                     T.box_hh.as<double>(), T.box_r.as<double>(),
                                                     spec.s0, spec.seg);
