@@ -49,6 +49,8 @@ struct fmm2d_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   cudaStream_t own_st = nullptr;     // the stream this context created (st may be external)
+  cudaStream_t st_copy = nullptr;    // H2D of the inputs needed late (strengths, evaluation points)
+  cudaEvent_t ev_inputs = nullptr;
   TreePlan plan;
   TreeState T;
   ListState Ls;

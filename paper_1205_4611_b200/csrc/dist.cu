@@ -807,6 +807,7 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
     T.pos_p = D.loc_pos.as<double2>();
     T.g_p = D.loc_g.as<double>();
     T.epos_p = nullptr;
+    T.inputs_ready = nullptr;
     T.spec = TreeSpec{};
     T.spec.s0 = s0;
     T.spec.seg = rank;

@@ -100,6 +100,7 @@ struct TreeState {
   const double2* pos_p = nullptr;    // inputs actually used (owned copies or caller's
   const double* g_p = nullptr;       //   device memory), original order
   const double2* epos_p = nullptr;
+  cudaEvent_t inputs_ready = nullptr;  // strengths / evaluation points uploaded (host calls)
   DBuf keys_in, keys_out, vals_in, vals_out, cub_tmp;
   DBuf perm_x, perm_y, rank_x, rank_y;
   DBuf X0, X1, Y0, Y1;               // int2 (rank_x, rank_y) arrays

@@ -76,16 +76,20 @@ void set_inputs(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, int
   T.n = n;
   T.aliased = epos == nullptr;
   T.m = T.aliased ? n : m;
+  T.inputs_ready = nullptr;
   if (device_io) {
     T.pos_p = reinterpret_cast<const double2*>(pos);
     T.g_p = g;
     T.epos_p = reinterpret_cast<const double2*>(epos);
     return;
   }
+  // positions first on the compute stream (the tree starts with them); the
+  // strengths and evaluation points travel on a copy stream, overlapping the
+  // rank sorts, and run_tree waits for them just before their first use
   T.pos.reserve(sizeof(double2) * n);
   T.g.reserve(sizeof(double) * n);
   FMM_CUDA(cudaMemcpyAsync(T.pos.p, pos, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
-  FMM_CUDA(cudaMemcpyAsync(T.g.p, g, sizeof(double) * n, cudaMemcpyHostToDevice, c->st));
+  FMM_CUDA(cudaMemcpyAsync(T.g.p, g, sizeof(double) * n, cudaMemcpyHostToDevice, c->st_copy));
   *h2d += (sizeof(double2) + sizeof(double)) * n;
   T.pos_p = T.pos.as<double2>();
   T.g_p = T.g.as<double>();
@@ -93,10 +97,12 @@ void set_inputs(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, int
   if (!T.aliased) {
     T.epos.reserve(sizeof(double2) * m);
     FMM_CUDA(cudaMemcpyAsync(T.epos.p, epos, sizeof(double2) * m, cudaMemcpyHostToDevice,
-                             c->st));
+                             c->st_copy));
     *h2d += sizeof(double2) * m;
     T.epos_p = T.epos.as<double2>();
   }
+  FMM_CUDA(cudaEventRecord(c->ev_inputs, c->st_copy));
+  T.inputs_ready = c->ev_inputs;
 }
 
 // the degenerate box reported first by the reference: smallest level, then box
@@ -274,6 +280,8 @@ int fmm2d_create(fmm2d_ctx** out, int device) {
     FMM_CUDA(cudaSetDevice(device));
     FMM_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     c->own_st = c->st;
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_inputs, cudaEventDisableTiming));
     for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
     c->d_status.reserve(sizeof(DevStatus));
     FMM_CUDA(cudaMallocHost(&c->h_status, sizeof(DevStatus)));
@@ -300,6 +308,9 @@ void fmm2d_destroy(fmm2d_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_hist) cudaFreeHost(c->h_hist);
+  if (c->st_copy) cudaStreamSynchronize(c->st_copy);
+  if (c->ev_inputs) cudaEventDestroy(c->ev_inputs);
+  if (c->st_copy) cudaStreamDestroy(c->st_copy);
   if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
 }

@@ -744,6 +744,14 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   T.vals_in.reserve(sizeof(int) * nmx);
   T.vals_out.reserve(sizeof(int) * nmx);
 
+  // strengths / evaluation points uploaded on the copy stream: wait before their
+  // first use (the bounding box when evaluation points are separate)
+  bool inputs_waited = false;
+  auto wait_inputs = [&] {
+    if (T.inputs_ready && !inputs_waited) FMM_CUDA(cudaStreamWaitEvent(st, T.inputs_ready, 0));
+    inputs_waited = true;
+  };
+  if (!T.aliased) wait_inputs();
   // root rectangle: given (subtree of a distributed top split) or the tight bbox
   if (spec.root_given) {
     const Rect rr{spec.root[0], spec.root[1], spec.root[2], spec.root[3]};
@@ -825,6 +833,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       std::swap(yp, yq);
     }
     T.leaf_of.reserve(sizeof(int) * std::max(n, m));
+    wait_inputs();
     if (P.smem_bytes > 0) {
       SubArgs A{a, sb, S, X0, X1, Y0, Y1, xp, yp, T.perm_x.as<int>(), pos, T.g_p,
                 T.src_pos.as<double2>(), T.src_g.as<double>(), T.src_perm.as<int>(),
@@ -888,6 +897,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     }
   } else {
     // L == 0: a single box, identity permutations (tree.py:316-317)
+    wait_inputs();
     note_launch();
     launch(k_iota_perm, nblk(n, 256), 256, 0, st, T.vals_in.as<int>(), n);
     note_launch();
