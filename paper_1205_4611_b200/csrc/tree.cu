@@ -127,7 +127,8 @@ __global__ void k_make_keys(const double2* __restrict__ pos, long long n, int ax
 // stable sort by it orders the points up to runs of equal keys, which
 // k_fix_ties then orders exactly by (coordinate, index).
 __global__ void k_make_keys32(const double2* __restrict__ pos, long long n, int axis,
-                              const Rect* __restrict__ root, unsigned* keys, int* vals) {
+                              const Rect* __restrict__ root, unsigned* keys, int* vals,
+                              int shift) {
   pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -140,7 +141,7 @@ __global__ void k_make_keys32(const double2* __restrict__ pos, long long n, int 
     const double u = (c - lo) / span * 4294967296.0;
     k = u >= 4294967295.0 ? 0xffffffffu : (unsigned)u;
   }
-  keys[i] = k;
+  keys[i] = k >> shift;      // key_bits = 32 - shift (ties fixed exactly by k_fix_ties)
   vals[i] = (int)i;
 }
 
@@ -782,9 +783,14 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         auto* kin = reinterpret_cast<unsigned*>(T.keys_in.p);
         auto* kout = reinterpret_cast<unsigned*>(T.keys_out.p);
         note_launch();
+        // key resolution ~16x finer than the mean point spacing: a radix pass less
+        // for small N, equal-key runs stay short (k_fix_ties orders them exactly)
+        int nb = 0;
+        while ((1ll << nb) < n) ++nb;
+        const int key_bits = std::min(32, std::max(16, (nb + 4 + 7) / 8 * 8));
         launch(k_make_keys32, nblk(n, 256), 256, 0, st, pos, n, axis, T.rect_tab.as<Rect>(), kin,
-                                                    T.vals_in.as<int>());
-        radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 32, st);
+               T.vals_in.as<int>(), 32 - key_bits);
+        radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, key_bits, st);
         note_launch();
         launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, dstat);
       }
