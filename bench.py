@@ -57,6 +57,17 @@ def p2p_flops_per_interaction():
 HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)
 
 
+def ncu_traffic(kernel, config):
+    """dram__bytes_read + dram__bytes_write of one launch of `kernel` from the
+    committed ncu capture (profiles/r01/ncu_traffic.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r01" / "ncu_traffic.json").read_text())
+        t = d[kernel][config]
+        return int(t["dram_read"] + t["dram_write"])
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -283,7 +294,8 @@ def run_ours(args, cfg, ws, rank, local):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_mean * 1e3},
         "roofline": {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic("k_m2l_dense", args.config),
                      "algorithmic": f"{pairs} M2L pairs x {m2l_flops_per_pair(cfg['p'])} flop "
                                     "(SURVEY 8(d)) per launch / M2L phase event time",
                      "peak_source": peak_src},
