@@ -398,13 +398,22 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
     const cplx q{-inv.x, -inv.y};
     double ax[PM], ay[PM];
     {
-      cplx pw = q;
+      // powers q^k as four interleaved chains (stride q^4): the serial
+      // dependency of the prescale drops from PM to ~PM/4 complex products
+      const cplx q2 = cmul(q, q);
+      cplx pw[4] = {q, q2, cmul(q2, q), cmul(q2, q2)};
+      const cplx q4 = pw[3];
 #pragma unroll
-      for (int k = 1; k <= PM; ++k) {
-        const cplx v = cmul(cplx{P.a[k - 1].x, P.a[k - 1].y}, pw);
-        ax[k - 1] = v.x;
-        ay[k - 1] = v.y;
-        pw = cmul(pw, q);
+      for (int k = 1; k <= PM; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k + u <= PM) {
+            const cplx v = cmul(cplx{P.a[k + u - 1].x, P.a[k + u - 1].y}, pw[u]);
+            ax[k + u - 1] = v.x;
+            ay[k + u - 1] = v.y;
+            pw[u] = cmul(pw[u], q4);
+          }
+        }
       }
     }
     // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
