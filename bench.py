@@ -293,7 +293,11 @@ def run_ours(args, cfg, ws, rank, local):
         "e2e": {"value": ws * n / e2e_mean, "unit": "particles/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_mean * 1e3},
-        "roofline": {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "peak": peak,
+        # compute roof: on B200 the FP64 tensor (DMMA) peak equals the DFMA vector
+        # peak (one shared FP64 pipe, profiles/r01_fp64_peak.json); the kernel
+        # runs on the vector pipe
+        "roofline": {"kernel": "m2l", "bound": "tensor", "pipe": "fp64 (DMMA = DFMA peak)",
+                     "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("k_m2l_dense", args.config),
                      "algorithmic": f"{pairs} M2L pairs x {m2l_flops_per_pair(cfg['p'])} flop "
@@ -413,7 +417,8 @@ def run_dist(args, cfg, ws, rank, local):
         "e2e": {"value": n_total / e2e_s, "unit": "particles/s",
                 "h2d_bytes_per_step": 24 * (hi - lo), "d2h_bytes_per_step": 24 * len(own),
                 "ms_per_step": e2e_s * 1e3},
-        "roofline": {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "peak": peak,
+        "roofline": {"kernel": "m2l", "bound": "tensor", "pipe": "fp64 (DMMA = DFMA peak)",
+                     "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                      "algorithmic": f"rank-0 M2L pairs {pairs} x {m2l_flops_per_pair(cfg['p'])} "
                                     "flop / slowest rank's M2L phase time"},
