@@ -531,7 +531,7 @@ def main():
     ws, rank, local = dist_env()
     if args.impl == "reference":
         out = run_reference(args, cfg, ws, rank)
-    elif ws > 1:
+    elif ws > 1 or os.environ.get("FMM2D_FORCE_DIST") == "1":
         out = run_dist(args, cfg, ws, rank, local)
     else:
         out = run_ours(args, cfg, ws, rank, local)

@@ -52,7 +52,6 @@ def engine_run(spec, out):
     import paper_1205_4611_b200 as F
     from paper_1205_4611_b200.distributed import fmm_evaluate_distributed
     _, kind, n, p = spec.split(":")
-    torch.cuda.set_device(0)
     pts = F.sample_points(F.DistributionSpec(kind, 0.01, 7), int(n))
     cfg = F.TreeConfig(35, 0.5, int(p))
     vals, rep = fmm_evaluate_distributed(pts, cfg, device=0)
@@ -66,9 +65,17 @@ def engine_run(spec, out):
 
 
 def main():
+    import torch
     import torch.distributed as dist
     mode, out = sys.argv[1], sys.argv[2]
-    dist.init_process_group("gloo")
+    if mode.startswith("engine-nccl"):
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+        mode = "engine" + mode[len("engine-nccl"):]
+    else:
+        if mode != "comm":
+            torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
     try:
         if mode == "comm":
             comm_checks(out)

@@ -66,3 +66,22 @@ def test_distributed_matches_single_gpu(tmp_path, world, kind, n, p):
     assert drep["skips"] == rep.coincident_skips
     assert drep["hist"] == {k: {str(a): b for a, b in v.items()}
                             for k, v in rep.list_histograms.items()}
+
+
+@pytest.mark.gpu
+def test_distributed_nccl_single_rank(tmp_path):
+    """The NCCL (non-staged) collective path of the distributed engine, run
+    with one rank (a single-GPU box cannot host two NCCL ranks)."""
+    import paper_1205_4611_b200 as F
+    out = tmp_path / "nccl.npz"
+    env = dict(os.environ, PYTHONPATH=str(ROOT), FMM2D_DIST_BACKEND="nccl")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29677", str(WORKER),
+           "engine-nccl:uniform:30000:20", str(out)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    d = np.load(out)
+    pts = F.sample_points(F.DistributionSpec("uniform", 0.01, 7), 30000)
+    ref, rep = F.fmm_evaluate(pts, F.TreeConfig(35, 0.5, 20), device=0)
+    assert np.max(np.abs(d["values"] - ref) / np.abs(ref)) <= 1e-13
+    assert json.loads(str(d["report"]))["totals"] == rep.list_totals
