@@ -298,30 +298,58 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 // coefficient and segment, coalesced row updates).  Targets wholly inside
 // the item are updated in place (exclusive owner, no atomics); targets whose
 // pairs span items leave ordered partials for k_m2l_fixup.
+#ifndef M2L_KOUTER
+#define M2L_KOUTER 0
+#endif
 constexpr int M2L_ITEM = 128;
-constexpr int PASCAL_N = 64;
 
-struct PascalTab {
-  double v[PASCAL_N][PASCAL_N];
+// Per-order table T[j][k-1] = C(j+k-1, k-1), j = 0..PM, k = 1..PM, rows of
+// even stride so consecutive k pairs are one 16-byte uniform constant load;
+// the ~3 KB an order uses stays resident in the SM's constant cache.
+template <int PM>
+struct M2LTab {
+  static constexpr int STRIDE = (PM + 1) & ~1;
+  double v[PM + 1][STRIDE];
 };
-constexpr PascalTab make_pascal() {
-  PascalTab t{};
-  unsigned long long row[PASCAL_N] = {};
-  for (int n = 0; n < PASCAL_N; ++n) {
+template <int PM>
+constexpr M2LTab<PM> make_m2l_tab() {
+  M2LTab<PM> t{};
+  unsigned long long row[2 * PM + 1] = {};
+  double pas[2 * PM][2 * PM] = {};
+  for (int n = 0; n < 2 * PM; ++n) {
     for (int k = n; k >= 1; --k) row[k] += row[k - 1];   // C(n, k), exact in u64 for n < 64
     row[0] = 1;
-    for (int k = 0; k < PASCAL_N; ++k) t.v[n][k] = k <= n ? (double)row[k] : 0.0;
+    for (int k = 0; k <= n; ++k) pas[n][k] = (double)row[k];
   }
+  for (int j = 0; j <= PM; ++j)
+    for (int k = 1; k <= PM; ++k) t.v[j][k - 1] = pas[j + k - 1][k - 1];
   return t;
 }
-__constant__ PascalTab c_pascal = make_pascal();
+template <int PM>
+__constant__ __align__(16) M2LTab<PM> c_m2l_tab = make_m2l_tab<PM>();
+
+// FMA kept in program order by the front end (volatile asm), so the k-outer
+// schedule below reaches ptxas as written
+__device__ __forceinline__ double fma_ord(double a, double b, double c) {
+#if M2L_KOUTER == 2
+  double d;
+  asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(a), "d"(b), "d"(c));
+  return d;
+#else
+  return fma(a, b, c);
+#endif
+}
 
 template <int PM>
 struct M2LDenseCfg {
   static constexpr int R = 2 * (PM + 1);          // SMEM rows (re/im per coefficient)
   static constexpr int STR = M2L_ITEM + 1;        // odd row stride: conflict-free
   static constexpr int SMEM = R * STR * 8;
+#ifdef M2L_MINB
+  static constexpr int MINB = PM <= 20 ? M2L_MINB : (PM <= 24 ? 3 : 2);
+#else
   static constexpr int MINB = PM <= 20 ? 4 : (PM <= 24 ? 3 : 2);
+#endif
 };
 
 // one coalesced row update of a target segment's sum (coefficient j, part comp)
@@ -369,7 +397,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
             const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
             double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
   pdl_enter();
-  static_assert(2 * PM <= PASCAL_N, "Pascal table too small for this order");
+  static_assert(PM <= 32, "dense M2L is compiled for PM <= 32");
   using Cfg = M2LDenseCfg<PM>;
   if (lists_overflowed(st)) return;
   extern __shared__ double red[];                 // [R][STR]
@@ -381,7 +409,15 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   const long long nitems = (npairs + M2L_ITEM - 1) / M2L_ITEM;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   M2LPair<PM> P;
+#if M2L_KOUTER
+  // one item per CTA: no item loop, so the Pascal constants stay constant-bank
+  // operands instead of being hoisted into (spilled) registers
+  {
+    const long long item = blockIdx.x;
+    if (item >= nitems) return;
+#else
   for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+#endif
     m2l_load_pair<PM>(P, item * M2L_ITEM + tid, npairs, w_src, w_tgt, mult, p);
     // targets just before / after the item (segments continuing across items)
     const int prev_t = item > 0 ? __ldg(w_tgt + item * M2L_ITEM - 1) : -1;
@@ -417,15 +453,45 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       }
     }
     // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
+#if M2L_KOUTER
+    {   // k-outer: 2(PM+1) independent accumulation chains at every step (same
+        // per-coefficient summation order over k)
+      double sx[PM + 1], sy[PM + 1];
+#pragma unroll
+      for (int k = 1; k <= PM; ++k) {
+#pragma unroll
+        for (int j = 0; j <= PM; ++j) {
+          if (k == 1) {
+            sx[j] = ax[0];                      // C(j, 0) = 1
+            sy[j] = ay[0];
+          } else {
+            sx[j] = fma_ord(c_m2l_tab<PM>.v[j][k - 1], ax[k - 1], sx[j]);
+            sy[j] = fma_ord(c_m2l_tab<PM>.v[j][k - 1], ay[k - 1], sy[j]);
+          }
+        }
+      }
+      cplx pw = inv;
+#pragma unroll
+      for (int j = 0; j <= PM; ++j) {
+        cplx b{sx[j], sy[j]};
+        if (j > 0) {
+          b = cmul(b, pw);
+          pw = cmul(pw, inv);
+        }
+        red[(2 * j) * Cfg::STR + tid] = b.x;
+        red[(2 * j + 1) * Cfg::STR + tid] = b.y;
+      }
+    }
+#else
     {
       cplx pw = inv;
 #pragma unroll
       for (int j = 0; j <= PM; ++j) {
-        double sx = c_pascal.v[j][0] * ax[0], sy = c_pascal.v[j][0] * ay[0];
+        double sx = ax[0], sy = ay[0];                 // C(j, 0) = 1
 #pragma unroll
         for (int k = 2; k <= PM; ++k) {
-          sx = fma(c_pascal.v[j + k - 1][k - 1], ax[k - 1], sx);
-          sy = fma(c_pascal.v[j + k - 1][k - 1], ay[k - 1], sy);
+          sx = fma(c_m2l_tab<PM>.v[j][k - 1], ax[k - 1], sx);
+          sy = fma(c_m2l_tab<PM>.v[j][k - 1], ay[k - 1], sy);
         }
         cplx b{sx, sy};
         if (j > 0) {
@@ -436,6 +502,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
         red[(2 * j + 1) * Cfg::STR + tid] = b.y;
       }
     }
+#endif
     s_t[tid] = t;
     __syncthreads();
     // segment starts (pairs are sorted by target)
@@ -775,7 +842,7 @@ struct Launch {
     const int L = T.L;
     if (L == 0) return;
     const int* total = Ls.weak_off.as<int>() + level_base(L + 1);
-    if constexpr (2 * PM > PASCAL_N) {
+    if constexpr (PM > 32) {
       launch_target(T, Ls, E, dstat, st);
     } else {
       if (m2l_force_target()) {
@@ -793,7 +860,8 @@ struct Launch {
                                       Cfg::SMEM));
         attr = true;
       }
-      const unsigned grid = (unsigned)std::min<long long>(std::max(1ll, items),
+      const unsigned grid = M2L_KOUTER ? (unsigned)std::max(1ll, items)
+                                       : (unsigned)std::min<long long>(std::max(1ll, items),
                                                           (long long)Cfg::MINB * sm_count());
       note_launch();
       launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st, 

@@ -21,6 +21,9 @@ namespace {
 constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
+#ifndef P2P_HI
+#define P2P_HI 1
+#endif
 
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -53,11 +56,26 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
                                          double& bx, double& by, int& skips) {
   const double dx = zx - yx, dy = zy - yy;
   double r2 = fma(dx, dx, dy * dy);
+#if P2P_HI
+  // r2 >= 0, so its high word is zero only for 0 or a denormal (which
+  // rcp.approx.ftz cannot invert either): one 32-bit test selects the seed
+  // of 1/1 instead; the Newton step then sees r2 = 0 and returns 3 y, a
+  // finite factor on dx = dy = 0.  The skip count is one predicated add.
+  int hi = __double2hiint(r2);
+  asm("{\n\t.reg .pred z;\n\tsetp.eq.s32 z, %1, 0;\n\t@z add.s32 %0, %0, 1;\n\t"
+      "selp.b32 %1, 1072693248, %1, z;\n\t}"
+      : "+r"(skips), "+r"(hi));
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(__hiloint2double(hi, 0)));
+  const double e = fma(-r2, y, 1.0);
+  const double gs = g * fma(fma(e, e, e), y, y);
+#else
   const long long bits = __double_as_longlong(r2);
   const bool zero = bits == 0;
   skips += zero;
   r2 = zero ? 1.0 : r2;
   const double gs = g * rcp_nr(r2);
+#endif
   bx = fma(gs, dx, bx);
   by = fma(gs, dy, by);
 }
