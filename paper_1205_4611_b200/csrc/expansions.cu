@@ -298,9 +298,6 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 // coefficient and segment, coalesced row updates).  Targets wholly inside
 // the item are updated in place (exclusive owner, no atomics); targets whose
 // pairs span items leave ordered partials for k_m2l_fixup.
-#ifndef M2L_KOUTER
-#define M2L_KOUTER 0
-#endif
 constexpr int M2L_ITEM = 128;
 
 // Per-order table T[j][k-1] = C(j+k-1, k-1), j = 0..PM, k = 1..PM, rows of
@@ -327,18 +324,6 @@ constexpr M2LTab<PM> make_m2l_tab() {
 }
 template <int PM>
 __constant__ __align__(16) M2LTab<PM> c_m2l_tab = make_m2l_tab<PM>();
-
-// FMA kept in program order by the front end (volatile asm), so the k-outer
-// schedule below reaches ptxas as written
-__device__ __forceinline__ double fma_ord(double a, double b, double c) {
-#if M2L_KOUTER == 2
-  double d;
-  asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(a), "d"(b), "d"(c));
-  return d;
-#else
-  return fma(a, b, c);
-#endif
-}
 
 template <int PM>
 struct M2LDenseCfg {
@@ -409,15 +394,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   const long long nitems = (npairs + M2L_ITEM - 1) / M2L_ITEM;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   M2LPair<PM> P;
-#if M2L_KOUTER
-  // one item per CTA: no item loop, so the Pascal constants stay constant-bank
-  // operands instead of being hoisted into (spilled) registers
-  {
-    const long long item = blockIdx.x;
-    if (item >= nitems) return;
-#else
   for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-#endif
     m2l_load_pair<PM>(P, item * M2L_ITEM + tid, npairs, w_src, w_tgt, mult, p);
     // targets just before / after the item (segments continuing across items)
     const int prev_t = item > 0 ? __ldg(w_tgt + item * M2L_ITEM - 1) : -1;
@@ -453,36 +430,6 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       }
     }
     // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
-#if M2L_KOUTER
-    {   // k-outer: 2(PM+1) independent accumulation chains at every step (same
-        // per-coefficient summation order over k)
-      double sx[PM + 1], sy[PM + 1];
-#pragma unroll
-      for (int k = 1; k <= PM; ++k) {
-#pragma unroll
-        for (int j = 0; j <= PM; ++j) {
-          if (k == 1) {
-            sx[j] = ax[0];                      // C(j, 0) = 1
-            sy[j] = ay[0];
-          } else {
-            sx[j] = fma_ord(c_m2l_tab<PM>.v[j][k - 1], ax[k - 1], sx[j]);
-            sy[j] = fma_ord(c_m2l_tab<PM>.v[j][k - 1], ay[k - 1], sy[j]);
-          }
-        }
-      }
-      cplx pw = inv;
-#pragma unroll
-      for (int j = 0; j <= PM; ++j) {
-        cplx b{sx[j], sy[j]};
-        if (j > 0) {
-          b = cmul(b, pw);
-          pw = cmul(pw, inv);
-        }
-        red[(2 * j) * Cfg::STR + tid] = b.x;
-        red[(2 * j + 1) * Cfg::STR + tid] = b.y;
-      }
-    }
-#else
     {
       cplx pw = inv;
 #pragma unroll
@@ -502,7 +449,6 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
         red[(2 * j + 1) * Cfg::STR + tid] = b.y;
       }
     }
-#endif
     s_t[tid] = t;
     __syncthreads();
     // segment starts (pairs are sorted by target)
@@ -860,8 +806,7 @@ struct Launch {
                                       Cfg::SMEM));
         attr = true;
       }
-      const unsigned grid = M2L_KOUTER ? (unsigned)std::max(1ll, items)
-                                       : (unsigned)std::min<long long>(std::max(1ll, items),
+      const unsigned grid = (unsigned)std::min<long long>(std::max(1ll, items),
                                                           (long long)Cfg::MINB * sm_count());
       note_launch();
       launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st, 

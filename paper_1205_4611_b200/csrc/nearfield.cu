@@ -21,6 +21,9 @@ namespace {
 constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
+#ifndef P2P_SCAN
+#define P2P_SCAN 1
+#endif
 #ifndef P2P_HI
 #define P2P_HI 1
 #endif
@@ -82,9 +85,10 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
 
 // One warp per target leaf.  The leaf's near sources (the concatenated source
 // ranges of its p2p boxes, ascending) are staged into a per-warp SMEM buffer
-// with cp.async; the box table (ids, ranges, running offsets) is fetched once
-// per 32 boxes with coalesced loads and walked by shuffles, so staging costs
-// no dependent global round trips per box.  With n_e points in the current
+// with cp.async; the box table (ids, ranges) is fetched once per 32 boxes
+// with coalesced loads and a warp scan of the counts maps every staged slot
+// to its box, so staging costs one copy per lane per 32 sources and no
+// dependent global round trips per box.  With n_e points in the current
 // block of <= 32, G = 32/n_e lane groups share each point; group k sums a
 // CONTIGUOUS slice of the staged sources (immediate-offset SMEM reads,
 // 4-way unrolled, two accumulator pairs), then the G partial sums are folded
@@ -118,6 +122,56 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
     int qb = q0, ib = 0;
     while (qb < q1) {
       int fill = 0;
+#if P2P_SCAN
+      // one group of <= 32 boxes per step: lane k holds box k's range, an
+      // inclusive warp scan of the counts maps every staged slot to its box
+      // (5-step shuffle search), so each lane issues one copy per 32 sources
+      // instead of the warp walking the boxes one by one
+      while (qb < q1 && fill < P2P_CHUNK) {
+        const int nq = min(32, q1 - qb);
+        int bs0 = 0, bcnt = 0;
+        if (lane < nq) {
+          const int a = n_idx[qb + lane];
+          bs0 = soff[a];
+          bcnt = soff[a + 1] - bs0;
+          if (lane == 0) { bs0 += ib; bcnt -= ib; }
+        }
+        int incl = bcnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int take = min(total, P2P_CHUNK - fill);
+        const int src_base = bs0 - (incl - bcnt);     // source of slot t in box k: src_base_k + t
+        for (int t0 = 0; t0 < take; t0 += 32) {     // warp-uniform trip count
+          const int t = t0 + lane;
+          int k = 0;
+#pragma unroll
+          for (int st = 16; st; st >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, k + st - 1);
+            if (v <= t) k += st;
+          }
+          const int src = __shfl_sync(0xffffffffu, src_base, k & 31) + t;
+          if (t < take) {
+            cp_async16(sp + fill + t, src_pos + src);
+            cp_async8(sg + fill + t, src_g + src);
+          }
+        }
+        fill += take;
+        if (take < total) {        // chunk full inside box k: resume there next round
+          const unsigned over = __ballot_sync(0xffffffffu, incl > take);
+          const int k = __ffs(over) - 1;
+          const int excl_k = __shfl_sync(0xffffffffu, incl - bcnt, k);
+          ib = (k == 0 ? ib : 0) + (take - excl_k);
+          qb += k;
+          break;
+        }
+        qb += nq;
+        ib = 0;
+      }
+#else
       bool partial = false;
       while (qb < q1 && fill < P2P_CHUNK && !partial) {
         const int nq = min(32, q1 - qb);
@@ -147,6 +201,7 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
         qb += k;
         if (!partial) ib = 0;
       }
+#endif
       cp_async_wait_all();
       __syncwarp();
       if (active) {
