@@ -126,42 +126,82 @@ __global__ void k_make_keys(const double2* __restrict__ pos, long long n, int ax
 // rectangle.  Non-decreasing in c (every step rounds monotonically), so a
 // stable sort by it orders the points up to runs of equal keys, which
 // k_fix_ties then orders exactly by (coordinate, index).
-__global__ void k_make_keys32(const double2* __restrict__ pos, long long n, int axis,
+__global__ void k_make_keys32(const double2* __restrict__ pos, long long n,
                               const Rect* __restrict__ root, unsigned* keys, int* vals,
                               int shift) {
   pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Rect r = *root;
-  const double lo = axis ? r.y0 : r.x0, span = axis ? r.y1 - r.y0 : r.x1 - r.x0;
   const double2 z = pos[i];
-  const double c = axis ? z.y : z.x;
-  unsigned k = 0;
-  if (span > 0.0) {
-    const double u = (c - lo) / span * 4294967296.0;
-    k = u >= 4294967295.0 ? 0xffffffffu : (unsigned)u;
+  // both axes in one pass: x keys in keys[0, n), y keys in keys[n, 2n)
+#pragma unroll
+  for (int axis = 0; axis < 2; ++axis) {
+    const double lo = axis ? r.y0 : r.x0, span = axis ? r.y1 - r.y0 : r.x1 - r.x0;
+    const double c = axis ? z.y : z.x;
+    unsigned k = 0;
+    if (span > 0.0) {
+      const double u = (c - lo) / span * 4294967296.0;
+      k = u >= 4294967295.0 ? 0xffffffffu : (unsigned)u;
+    }
+    keys[axis * n + i] = k >> shift;   // key_bits = 32 - shift (ties fixed exactly by k_fix_ties)
   }
-  keys[i] = k >> shift;      // key_bits = 32 - shift (ties fixed exactly by k_fix_ties)
   vals[i] = (int)i;
 }
 
 constexpr int TIE_RUN_MAX = 64;
 
-// order every run of equal 32-bit keys by (coordinate, original index); a run
-// longer than TIE_RUN_MAX (pathologically clustered input) raises
-// ST_RANK_RETRY and the host reruns with exact 64-bit keys
+// order every run of equal 32-bit keys by (coordinate, original index) and
+// write the inverse permutation (rank of every point along the axis) in the
+// same pass: singletons scatter their rank directly, a run's head thread
+// sorts the run and scatters its members' ranks.  A run longer than
+// TIE_RUN_MAX (pathologically clustered input) raises ST_RANK_RETRY and the
+// host reruns with exact 64-bit keys.
+//
+// The y pass (X != null) writes the split records directly instead of
+// rank_y: a point of y rank r and x rank rx is (rx, r) at Y[r] and X[rx]
+// (what k_init_arrays builds from both rank arrays in the exact-key path).
+struct RankOut {
+  int* rank;                 // x pass: rank along the axis
+  const int* rank_x;         // y pass: x ranks ...
+  int2* X;                   // ... and the two record copies
+  int2* Y;
+  unsigned char* xpar;
+  unsigned char* ypar;
+};
+__device__ __forceinline__ void emit_rank(const RankOut& o, int idx, int r, long long n) {
+  if (o.X) {
+    const int rx = o.rank_x[idx];
+    o.Y[r] = make_int2(rx, r);
+    // rank_x is incomplete only when the x pass raised ST_RANK_RETRY (the
+    // build is then redone with exact keys): never scatter out of range
+    if ((unsigned long long)rx < (unsigned long long)n) o.X[rx] = make_int2(rx, r);
+  } else {
+    o.rank[idx] = r;
+  }
+}
+
 __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
-                           const double2* __restrict__ pos, int axis, long long n,
+                           const double2* __restrict__ pos, int axis, long long n, RankOut o,
                            DevStatus* st) {
   pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (i == 0 && o.X) { o.xpar[0] = 0; o.ypar[0] = 0; }
   const unsigned k = keys[i];
-  if ((i > 0 && keys[i - 1] == k) || i + 1 >= n || keys[i + 1] != k) return;
+  if (i > 0 && keys[i - 1] == k) return;                 // run member: the head writes it
+  if (i + 1 >= n || keys[i + 1] != k) {                  // singleton
+    emit_rank(o, perm[i], (int)i, n);
+    return;
+  }
   long long e = i + 1;
   while (e < n && keys[e] == k) {
     if (++e - i > TIE_RUN_MAX) {
       atomicOr(&st->flags, ST_RANK_RETRY);
+      // still emit a valid (if not exactly ordered) permutation, so the rest
+      // of this attempt indexes in bounds before the host reruns it
+      while (e < n && keys[e] == k) ++e;
+      for (long long q = i; q < e; ++q) emit_rank(o, perm[q], (int)q, n);
       return;
     }
   }
@@ -185,7 +225,10 @@ __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
     idx[r + 1] = vi;
     crd[r + 1] = vc;
   }
-  for (int q = 0; q < cnt; ++q) perm[i + q] = idx[q];
+  for (int q = 0; q < cnt; ++q) {
+    perm[i + q] = idx[q];
+    emit_rank(o, idx[q], (int)(i + q), n);
+  }
 }
 
 // inverse permutation: rank of every point along the sorted axis (an
@@ -771,6 +814,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   if (S > 0) {
     // global ranks along x and y (ties by original index: stable radix sort)
     for (DBuf* b : {&T.perm_x, &T.perm_y, &T.rank_x, &T.rank_y}) b->reserve(sizeof(int) * n);
+    for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
+    const long long pmax = (1ll << std::max(sb, 1)) + 2;
+    for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
     for (int axis = 0; axis < 2; ++axis) {
       int* perm = axis ? T.perm_y.as<int>() : T.perm_x.as<int>();
       if (T.exact_keys) {
@@ -780,32 +826,36 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         launch(k_make_keys, nblk(n, 256), 256, 0, st, pos, n, axis, kin, T.vals_in.as<int>());
         radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, 64, st);
       } else {
-        auto* kin = reinterpret_cast<unsigned*>(T.keys_in.p);
+        auto* kin = reinterpret_cast<unsigned*>(T.keys_in.p) + axis * n;   // 2n u32 fit
         auto* kout = reinterpret_cast<unsigned*>(T.keys_out.p);
-        note_launch();
         // key resolution ~16x finer than the mean point spacing: a radix pass less
         // for small N, equal-key runs stay short (k_fix_ties orders them exactly)
         int nb = 0;
         while ((1ll << nb) < n) ++nb;
         const int key_bits = std::min(32, std::max(16, (nb + 4 + 7) / 8 * 8));
-        launch(k_make_keys32, nblk(n, 256), 256, 0, st, pos, n, axis, T.rect_tab.as<Rect>(), kin,
-               T.vals_in.as<int>(), 32 - key_bits);
+        if (axis == 0) {
+          note_launch();
+          launch(k_make_keys32, nblk(n, 256), 256, 0, st, pos, n, T.rect_tab.as<Rect>(), kin,
+                 T.vals_in.as<int>(), 32 - key_bits);
+        }
         radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, key_bits, st);
         note_launch();
-        launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, dstat);
+        RankOut o{T.rank_x.as<int>(), nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (axis == 1)
+          o = RankOut{nullptr, T.rank_x.as<int>(), T.X0.as<int2>(), T.Y0.as<int2>(),
+                      T.xpar0.as<unsigned char>(), T.ypar0.as<unsigned char>()};
+        launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, o, dstat);
+        continue;
       }
       note_launch();
       launch(k_rank_scatter, nblk(n, 256), 256, 0, st, n, perm, axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
     }
-    for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
-    const long long pmax = (1ll << std::max(sb, 1)) + 2;
-    for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
-    note_launch();
-    launch(k_init_arrays, nblk(n, 256), 256, 0, st, n, T.perm_x.as<int>(), T.perm_y.as<int>(),
-                                                T.rank_x.as<int>(), T.rank_y.as<int>(),
-                                                T.X0.as<int2>(), T.Y0.as<int2>(),
-                                                T.xpar0.as<unsigned char>(),
-                                                T.ypar0.as<unsigned char>());
+    if (T.exact_keys) {
+      note_launch();
+      launch(k_init_arrays, nblk(n, 256), 256, 0, st, n, T.perm_x.as<int>(), T.perm_y.as<int>(),
+             T.rank_x.as<int>(), T.rank_y.as<int>(), T.X0.as<int2>(), T.Y0.as<int2>(),
+             T.xpar0.as<unsigned char>(), T.ypar0.as<unsigned char>());
+    }
     StepArgs a{P.d_off.as<int>(), T.rect_tab.as<Rect>(), T.cut_tab.as<double>(),
                T.axis_tab.as<unsigned char>(), pos, T.perm_x.as<int>(), T.perm_y.as<int>(),
                L, spec.s0, spec.seg};
