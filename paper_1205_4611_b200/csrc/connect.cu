@@ -13,6 +13,8 @@
 // which is also the pair list the single M2L launch consumes.  No host sync:
 // list buffers are sized from capacities kept in the context, and a fill that
 // would overflow only raises ST_OVERFLOW (the host then regrows and reruns).
+#include <cstdlib>
+
 #include "engine.h"
 #include "lookback.cuh"
 
@@ -31,6 +33,17 @@ constexpr int CL_WARPS = 8;     // warps per CTA
 constexpr int CL_PPW = 1;       // classify: parents (4 sibling targets each) per warp
 constexpr int CL_TPW = 8;       // reclassify: finest targets per warp
 constexpr int CL_MAXM = 16;     // ballot masks cached per target (512 candidates)
+#ifndef CL_SPLIT_MIN
+#define CL_SPLIT_MIN 1024       // parents per level from which the split classify runs
+#endif
+// split classify (predicates, then look-back + fill) unless FMM2D_CL_SPLIT=0
+bool cl_split() {
+  static bool v = [] {
+    const char* e = getenv("FMM2D_CL_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 // One level of classify_level (connectivity.py:47-68) in ONE pass.  A warp
 // walks CL_PPW parent boxes; for each it evaluates the four children against
@@ -207,6 +220,193 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
         wpos[j] += __popc(m);
         spos[j] += __popc(sm);
       }
+    }
+  }
+}
+
+// Split form of one classify_level (default): the predicate pass and the
+// list fill are separate launches, so the look-back that places every
+// target's lists runs on counts that are already known.  In the one-pass
+// kernel above a tile can only publish its count after its own predicates,
+// and on clustered inputs (long, uneven candidate lists) a slow tile stalls
+// every later tile in the look-back; here each fill tile publishes at once.
+//
+// k_classify_pred: one warp per parent (grid-stride), the four siblings'
+// far masks for each 32-candidate chunk go to global planes (word base of
+// parent P: (P - P0) + 4 * (ps_off[P] - ps_off[P0]) / 32, disjoint because
+// a parent needs at most 1 + floor(4 n_P / 32) words), counts to cnt[].
+__device__ __forceinline__ long long cl_wbase(const int* ps_off, long long P, long long P0) {
+  return (P - P0) + (4ll * (ps_off[P] - ps_off[P0])) / 32;
+}
+
+__global__ void __launch_bounds__(256)
+k_classify_pred(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
+                const int* __restrict__ ps_idx, long long P0, long long P1, long long tb,
+                long long te, int2* cnt, unsigned* masks, long long mplane, DevStatus* st) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(l);
+  const bool dead = lists_overflowed(st);
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long P = P0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); P < P1;
+       P += nwarps) {
+    const int a0 = ps_off[P];
+    const int ncand = dead ? 0 : 4 * (ps_off[P + 1] - a0);
+    const long long wb = cl_wbase(ps_off, P, P0);
+    double rt[4], xt[4], yt[4];
+    bool own[4];
+    unsigned ownm = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      own[j] = 4 * P + j >= tb && 4 * P + j < te;
+      ownm |= (unsigned)own[j] << j;
+      const long long gb = lb + 4 * P + j;
+      rt[j] = geo.r[gb];
+      xt[j] = geo.cx[gb];
+      yt[j] = geo.cy[gb];
+    }
+    int nw[4] = {0, 0, 0, 0}, ns[4] = {0, 0, 0, 0};
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+      const int c = c0 + lane;
+      const bool valid = c < ncand;
+      const long long gc = lb + (valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0);
+      const double xc = geo.cx[gc], yc = geo.cy[gc], rc = geo.r[gc];
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      unsigned mk = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!own[j]) continue;                                   // warp-uniform
+        const bool far =
+            valid && well_separated_dz(rt[j], rc, xt[j] - xc, yt[j] - yc, theta);
+        const unsigned m = __ballot_sync(0xffffffffu, far);
+        if (lane == j) mk = m;
+        nw[j] += __popc(m);
+        ns[j] += __popc(vm & ~m);
+      }
+      if (lane < 4 && ((ownm >> lane) & 1)) masks[lane * mplane + wb + (c0 >> 5)] = mk;
+    }
+    if (lane < 4) {
+      int w = 0, s = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j == lane) { w = nw[j]; s = ns[j]; }
+      cnt[4 * (P - P0) + lane] = make_int2(w, s);     // zero for targets not owned
+    }
+  }
+}
+
+// k_classify_fill: CL_WARPS parents per tile; the tile's count total is
+// published to the look-back first, then the compacted lists are written
+// from the stored masks (ascending candidate order, as before).
+__global__ void __launch_bounds__(CL_WARPS * 32)
+k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx, int* so,
+                int* sidx, long long scap, int* woff, int* widx, int* wtgt, long long wcap,
+                LookbackState lbs, unsigned ntiles, long long P0, long long P1, long long tb,
+                long long te, const int2* __restrict__ cnt, const unsigned* __restrict__ masks,
+                long long mplane, DevStatus* st) {
+  pdl_enter();
+  __shared__ int s_cnt[CL_WARPS][4][2];
+  __shared__ long long s_excl[2];
+  __shared__ unsigned s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
+  __syncthreads();
+  const unsigned tile = s_tile;
+  const bool dead = lists_overflowed(st);
+  const long long lb = level_base(l);
+  const long long P = P0 + (long long)tile * CL_WARPS + w;
+  if (lane < 4) {
+    int2 c = make_int2(0, 0);
+    if (P < P1 && !dead) c = cnt[4 * (P - P0) + lane];
+    s_cnt[w][lane][0] = c.x;
+    s_cnt[w][lane][1] = c.y;
+  }
+  __syncthreads();
+  if (w == 0) {
+    long long agg[2] = {0, 0}, excl[2];
+    for (int q = 0; q < CL_WARPS * 4; ++q) {
+      agg[0] += (&s_cnt[0][0][0])[2 * q];
+      agg[1] += (&s_cnt[0][0][0])[2 * q + 1];
+    }
+    lb_prefix<2>(lbs, tile, agg, excl);
+    if (lane == 0) {
+      s_excl[0] = excl[0];
+      s_excl[1] = excl[1];
+    }
+  }
+  __syncthreads();
+  const long long wbase0 = woff[lb];
+  long long wb = wbase0 + s_excl[0], sb = s_excl[1];
+  for (int q = 0; q < w; ++q)
+    for (int j = 0; j < 4; ++j) {
+      wb += s_cnt[q][j][0];
+      sb += s_cnt[q][j][1];
+    }
+  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {   // totals: end of this level
+    long long wt = wb, stt = sb;
+    for (int j = 0; j < 4; ++j) {
+      wt += s_cnt[w][j][0];
+      stt += s_cnt[w][j][1];
+    }
+    so[4 * P1] = (int)stt;
+    woff[lb + 4 * P1] = (int)wt;
+    woff[level_base(l + 1)] = (int)wt;     // next level's base (same slot when P1 = 4^(l-1))
+  }
+  if (P >= P1) return;
+  long long wpos[4], spos[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    wpos[j] = wb;
+    spos[j] = sb;
+    wb += s_cnt[w][j][0];
+    sb += s_cnt[w][j][1];
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      so[4 * P + j] = (int)spos[j];
+      woff[lb + 4 * P + j] = (int)wpos[j];
+    }
+  }
+  if (dead) return;
+  if (wb > wcap || sb > scap) {
+    if (lane == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 1);
+    }
+    return;
+  }
+  const unsigned below = (1u << lane) - 1u;
+  const int a0 = ps_off[P];
+  const int ncand = 4 * (ps_off[P + 1] - a0);
+  const long long mw = cl_wbase(ps_off, P, P0);
+  bool own[4];
+  unsigned ownm = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    own[j] = 4 * P + j >= tb && 4 * P + j < te;
+    ownm |= (unsigned)own[j] << j;
+  }
+  for (int c0 = 0; c0 < ncand; c0 += 32) {
+    const int c = c0 + lane;
+    const bool valid = c < ncand;
+    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned mine =
+        lane < 4 && ((ownm >> lane) & 1) ? masks[lane * mplane + mw + (c0 >> 5)] : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!own[j]) continue;
+      const unsigned m = __shfl_sync(0xffffffffu, mine, j);
+      const unsigned sm = vm & ~m;
+      if ((m >> lane) & 1u) {
+        const long long o = wpos[j] + __popc(m & below);
+        widx[o] = (int)(lb + cand);
+        wtgt[o] = (int)(lb + 4 * P + j);
+      }
+      if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
+      wpos[j] += __popc(m);
+      spos[j] += __popc(sm);
     }
   }
 }
@@ -454,19 +654,39 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
 
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
   int* woff = Ls.weak_off.as<int>();
+  // split classify scratch: counts per target, four far-mask planes per level
+  const long long mplane = nleaf / 4 + Ls.cap_strong / 8 + 4;
+  if (cl_split()) {
+    Ls.cl_cnt.reserve(sizeof(int2) * (nleaf + 4));
+    Ls.cl_mask.reserve(sizeof(unsigned) * 4 * mplane);
+  }
   note_launch();
   launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
     const long long tb = part.lo(l), te = part.hi(l);
     const long long P0 = tb >> 2, P1 = (te + 3) >> 2;
-    const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
-    note_launch();
-    launch(k_classify, ntiles, CL_WARPS * 32, 0, st, 
-        l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
-        Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
-        Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, P0, P1,
-        tb, te, dstat);
+    if (cl_split() && P1 - P0 >= CL_SPLIT_MIN) {
+      const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS - 1) / CL_WARPS);
+      note_launch();
+      launch(k_classify_pred, std::min(nblk((P1 - P0) * 32, 256), 8u * 148u), 256, 0, st, l, geo,
+             theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), P0, P1, tb, te,
+             Ls.cl_cnt.as<int2>(), Ls.cl_mask.as<unsigned>(), mplane, dstat);
+      note_launch();
+      launch(k_classify_fill, ntiles, CL_WARPS * 32, 0, st, l, Ls.s_off[cur].as<int>(),
+             Ls.s_idx[cur].as<int>(), Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(),
+             Ls.cap_strong, woff, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak,
+             lbstate(), ntiles, P0, P1, tb, te, Ls.cl_cnt.as<int2>(),
+             Ls.cl_mask.as<unsigned>(), mplane, dstat);
+    } else {
+      const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
+      note_launch();
+      launch(k_classify, ntiles, CL_WARPS * 32, 0, st,
+          l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
+          Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
+          Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, P0, P1,
+          tb, te, dstat);
+    }
     cur = 1 - cur;
   }
   {

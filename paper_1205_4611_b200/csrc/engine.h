@@ -134,6 +134,7 @@ struct ListState {
   DBuf weak_idx, weak_tgt;           // int32 (source global id, target global id)
   DBuf s_off[2], s_idx[2];           // strong lists ping-pong (level-local ids)
   DBuf lb_flags, lb_vals, lb_ticket;  // single-pass look-back state of the list kernels
+  DBuf cl_cnt, cl_mask;              // split classify: per-target counts, far masks
   long long lb_tiles = 0;
   unsigned lb_epoch = 0;
   DBuf p2p_off, p2p_idx, p2l_off, p2l_idx, m2p_off, m2p_idx;  // finest, level-local ids
