@@ -545,6 +545,136 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
   }
 }
 
+// Split form of reclassify_finest (default, same reason as the split
+// classify): k_reclassify_pred stores the p2l / m2p kind masks of every
+// 32-source chunk (word base of target b: (b - tb) + (s_off[b] - s_off[tb]) /
+// 32) and the three counts; k_reclassify_fill publishes its tile's counts to
+// the look-back first and then writes the three compacted lists.
+__global__ void __launch_bounds__(256)
+k_reclassify_pred(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
+                  const int* __restrict__ s_idx, long long tb, long long te, int4* cnt,
+                  unsigned* masks, long long mplane, DevStatus* st) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(L);
+  const bool dead = lists_overflowed(st);
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long b = tb + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); b < te;
+       b += nwarps) {
+    const int a0 = s_off[b], a1 = dead ? a0 : s_off[b + 1];
+    const long long wb = (b - tb) + (s_off[b] - s_off[tb]) / 32;
+    const long long gt = lb + b;
+    const double rt = geo.r[gt], xt = geo.cx[gt], yt = geo.cy[gt];
+    int n0 = 0, n1 = 0, n2 = 0;
+    for (int c0 = a0; c0 < a1; c0 += 32) {
+      const int c = c0 + lane;
+      const bool valid = c < a1;
+      int kind = 0;   // 0 p2p, 1 p2l (larger source), 2 m2p (smaller source)
+      if (valid) {
+        const int src = s_idx[c];
+        const double rs = geo.r[lb + src];
+        const bool sw = well_separated_swapped_dz(rt, rs, xt - geo.cx[lb + src],
+                                                  yt - geo.cy[lb + src], theta);
+        const bool moved = sw && src != b && rs != rt;
+        kind = moved ? (rs > rt ? 1 : 2) : 0;
+      }
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      const unsigned ml = __ballot_sync(0xffffffffu, kind == 1);
+      const unsigned mm = __ballot_sync(0xffffffffu, kind == 2);
+      const int ch = (c0 - a0) >> 5;
+      if (lane == 0) masks[wb + ch] = ml;
+      if (lane == 1) masks[mplane + wb + ch] = mm;
+      n0 += __popc(vm & ~(ml | mm));
+      n1 += __popc(ml);
+      n2 += __popc(mm);
+    }
+    if (lane == 0) cnt[b - tb] = make_int4(n0, n1, n2, 0);
+  }
+}
+
+__global__ void __launch_bounds__(CL_WARPS * 32)
+k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx, int* o_p2p,
+                  int* i_p2p, long long cap_p2p, int* o_p2l, int* i_p2l, long long cap_p2l,
+                  int* o_m2p, int* i_m2p, long long cap_m2p, LookbackState lbs, unsigned ntiles,
+                  long long tb, long long te, const int4* __restrict__ cnt,
+                  const unsigned* __restrict__ masks, long long mplane, DevStatus* st) {
+  pdl_enter();
+  __shared__ int s_cnt[CL_WARPS][CL_TPW][3];
+  __shared__ long long s_excl[3];
+  __shared__ unsigned s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
+  __syncthreads();
+  const unsigned tile = s_tile;
+  const bool dead = lists_overflowed(st);
+  const long long bw = tb + ((long long)tile * CL_WARPS + w) * CL_TPW;
+  if (lane < CL_TPW) {
+    int4 c = make_int4(0, 0, 0, 0);
+    if (bw + lane < te && !dead) c = cnt[bw + lane - tb];
+    s_cnt[w][lane][0] = c.x;
+    s_cnt[w][lane][1] = c.y;
+    s_cnt[w][lane][2] = c.z;
+  }
+  __syncthreads();
+  if (w == 0) {
+    long long agg[3] = {0, 0, 0}, excl[3];
+    for (int q = 0; q < CL_WARPS * CL_TPW; ++q)
+      for (int k = 0; k < 3; ++k) agg[k] += (&s_cnt[0][0][0])[3 * q + k];
+    lb_prefix<3>(lbs, tile, agg, excl);
+    if (lane == 0)
+      for (int k = 0; k < 3; ++k) s_excl[k] = excl[k];
+  }
+  __syncthreads();
+  long long pos[3] = {s_excl[0], s_excl[1], s_excl[2]};
+  for (int q = 0; q < w; ++q)
+    for (int u = 0; u < CL_TPW; ++u)
+      for (int k = 0; k < 3; ++k) pos[k] += s_cnt[q][u][k];
+  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {
+    long long tot[3] = {pos[0], pos[1], pos[2]};
+    for (int u = 0; u < CL_TPW; ++u)
+      for (int k = 0; k < 3; ++k) tot[k] += s_cnt[w][u][k];
+    o_p2p[te] = (int)tot[0];
+    o_p2l[te] = (int)tot[1];
+    o_m2p[te] = (int)tot[2];
+  }
+  const unsigned below = (1u << lane) - 1u;
+  for (int u = 0; u < CL_TPW; ++u) {
+    const long long b = bw + u;
+    if (b >= te) break;
+    if (lane == 0) {
+      o_p2p[b] = (int)pos[0];
+      o_p2l[b] = (int)pos[1];
+      o_m2p[b] = (int)pos[2];
+    }
+    const int n0 = s_cnt[w][u][0], n1 = s_cnt[w][u][1], n2 = s_cnt[w][u][2];
+    if (!dead && pos[0] + n0 <= cap_p2p && pos[1] + n1 <= cap_p2l && pos[2] + n2 <= cap_m2p) {
+      const int a0 = s_off[b], a1 = s_off[b + 1];
+      const long long wb = (b - tb) + (a0 - s_off[tb]) / 32;
+      long long q0 = pos[0], q1 = pos[1], q2 = pos[2];
+      for (int c0 = a0; c0 < a1; c0 += 32) {
+        const int c = c0 + lane;
+        const int ch = (c0 - a0) >> 5;
+        const int src = c < a1 ? s_idx[c] : 0;
+        const unsigned vm = __ballot_sync(0xffffffffu, c < a1);
+        const unsigned ml = masks[wb + ch], mm = masks[mplane + wb + ch];
+        const unsigned mp = vm & ~(ml | mm);
+        if ((mp >> lane) & 1u) i_p2p[q0 + __popc(mp & below)] = src;
+        if ((ml >> lane) & 1u) i_p2l[q1 + __popc(ml & below)] = src;
+        if ((mm >> lane) & 1u) i_m2p[q2 + __popc(mm & below)] = src;
+        q0 += __popc(mp);
+        q1 += __popc(ml);
+        q2 += __popc(mm);
+      }
+    } else if (!dead && lane == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 2);
+    }
+    pos[0] += n0;
+    pos[1] += n1;
+    pos[2] += n2;
+  }
+}
+
 // off[i] for i outside the written window [lo, hi]: off[lo] before, off[hi] after
 __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
   pdl_enter();
@@ -655,10 +785,11 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
   int* woff = Ls.weak_off.as<int>();
   // split classify scratch: counts per target, four far-mask planes per level
-  const long long mplane = nleaf / 4 + Ls.cap_strong / 8 + 4;
+  const long long mplane = nleaf / 4 + Ls.cap_strong / 8 + 4;      // classify planes (4)
+  const long long rplane = nleaf + Ls.cap_strong / 32 + 4;          // reclassify planes (2)
   if (cl_split()) {
-    Ls.cl_cnt.reserve(sizeof(int2) * (nleaf + 4));
-    Ls.cl_mask.reserve(sizeof(unsigned) * 4 * mplane);
+    Ls.cl_cnt.reserve(sizeof(int4) * (nleaf + 4));
+    Ls.cl_mask.reserve(sizeof(unsigned) * std::max(4 * mplane, 2 * rplane));
   }
   note_launch();
   launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
@@ -692,12 +823,25 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   {
     const long long tb = part.lo(L), te = part.hi(L);
     const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
-    note_launch();
-    launch(k_reclassify, ntiles, CL_WARPS * 32, 0, st, 
-        L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),
-        Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
-        Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles,
-        tb, te, dstat);
+    if (cl_split() && te - tb >= 4 * CL_SPLIT_MIN) {
+      note_launch();
+      launch(k_reclassify_pred, std::min(nblk((te - tb) * 32, 256), 8u * 148u), 256, 0, st, L,
+             geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), tb, te,
+             Ls.cl_cnt.as<int4>(), Ls.cl_mask.as<unsigned>(), rplane, dstat);
+      note_launch();
+      launch(k_reclassify_fill, ntiles, CL_WARPS * 32, 0, st, Ls.s_off[cur].as<int>(),
+             Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), Ls.cap_p2p,
+             Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), Ls.cap_p2l, Ls.m2p_off.as<int>(),
+             Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles, tb, te, Ls.cl_cnt.as<int4>(),
+             Ls.cl_mask.as<unsigned>(), rplane, dstat);
+    } else {
+      note_launch();
+      launch(k_reclassify, ntiles, CL_WARPS * 32, 0, st,
+          L, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(),
+          Ls.p2p_idx.as<int>(), Ls.cap_p2p, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(),
+          Ls.cap_p2l, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles,
+          tb, te, dstat);
+    }
   }
   if (part.G > 1) {
     // empty lists for boxes this rank does not own: monotone CSR offsets
