@@ -295,118 +295,148 @@ k_classify_pred(int l, LevelGeo geo, double theta, const int* __restrict__ ps_of
   }
 }
 
-// k_classify_fill: CL_WARPS parents per tile; the tile's count total is
-// published to the look-back first, then the compacted lists are written
-// from the stored masks (ascending candidate order, as before).
-__global__ void __launch_bounds__(CL_WARPS * 32)
-k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx, int* so,
-                int* sidx, long long scap, int* woff, int* widx, int* wtgt, long long wcap,
-                LookbackState lbs, unsigned ntiles, long long P0, long long P1, long long tb,
-                long long te, const int2* __restrict__ cnt, const unsigned* __restrict__ masks,
-                long long mplane, DevStatus* st) {
+// Exclusive scan of NC per-entry counters (entry stride CS ints) into the
+// CSR offset arrays out[k][0..n] (+ *base for counter 0; the total also to
+// *tot_extra).  Large tiles (SCAN_TILE entries) keep the look-back chain short;
+// the counts are already known, so every tile publishes at once.
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8, SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+struct ScanOut {
+  int* out[3];
+  const int* base;          // added to counter 0 (null: 0)
+  int* tot_extra;           // also receives counter 0's total (null: none)
+};
+template <int NC, int CS>
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_counts(const int* __restrict__ cnt, long long n, ScanOut o, LookbackState lbs,
+              unsigned ntiles, DevStatus* st) {
   pdl_enter();
-  __shared__ int s_cnt[CL_WARPS][4][2];
-  __shared__ long long s_excl[2];
+  __shared__ long long s_w[SCAN_THREADS / 32][NC];
+  __shared__ long long s_excl[NC];
   __shared__ unsigned s_tile;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned tile = s_tile;
   const bool dead = lists_overflowed(st);
-  const long long lb = level_base(l);
-  const long long P = P0 + (long long)tile * CL_WARPS + w;
-  if (lane < 4) {
-    int2 c = make_int2(0, 0);
-    if (P < P1 && !dead) c = cnt[4 * (P - P0) + lane];
-    s_cnt[w][lane][0] = c.x;
-    s_cnt[w][lane][1] = c.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i0 = (long long)tile * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  int v[SCAN_ITEMS][NC];
+  long long tsum[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) tsum[k] = 0;
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q)
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      v[q][k] = (i0 + q < n && !dead) ? cnt[(i0 + q) * CS + k] : 0;
+      tsum[k] += v[q][k];
+    }
+  long long incl[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    incl[k] = tsum[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, incl[k], d);
+      if (lane >= d) incl[k] += t;
+    }
+    if (lane == 31) s_w[w][k] = incl[k];
   }
   __syncthreads();
   if (w == 0) {
-    long long agg[2] = {0, 0}, excl[2];
-    for (int q = 0; q < CL_WARPS * 4; ++q) {
-      agg[0] += (&s_cnt[0][0][0])[2 * q];
-      agg[1] += (&s_cnt[0][0][0])[2 * q + 1];
+    long long agg[NC], excl[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      agg[k] = 0;
+      for (int q = 0; q < SCAN_THREADS / 32; ++q) agg[k] += s_w[q][k];
     }
-    lb_prefix<2>(lbs, tile, agg, excl);
+    lb_prefix<NC>(lbs, tile, agg, excl);
     if (lane == 0) {
-      s_excl[0] = excl[0];
-      s_excl[1] = excl[1];
+      const long long b0 = o.base ? *o.base : 0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) s_excl[k] = excl[k] + (k == 0 ? b0 : 0);
+      if (tile == ntiles - 1) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) o.out[k][n] = (int)(s_excl[k] + agg[k]);
+        if (o.tot_extra) *o.tot_extra = (int)(s_excl[0] + agg[0]);
+      }
     }
   }
   __syncthreads();
-  const long long wbase0 = woff[lb];
-  long long wb = wbase0 + s_excl[0], sb = s_excl[1];
-  for (int q = 0; q < w; ++q)
-    for (int j = 0; j < 4; ++j) {
-      wb += s_cnt[q][j][0];
-      sb += s_cnt[q][j][1];
-    }
-  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {   // totals: end of this level
-    long long wt = wb, stt = sb;
-    for (int j = 0; j < 4; ++j) {
-      wt += s_cnt[w][j][0];
-      stt += s_cnt[w][j][1];
-    }
-    so[4 * P1] = (int)stt;
-    woff[lb + 4 * P1] = (int)wt;
-    woff[level_base(l + 1)] = (int)wt;     // next level's base (same slot when P1 = 4^(l-1))
-  }
-  if (P >= P1) return;
-  long long wpos[4], spos[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    wpos[j] = wb;
-    spos[j] = sb;
-    wb += s_cnt[w][j][0];
-    sb += s_cnt[w][j][1];
-  }
-  if (lane == 0) {
+  for (int k = 0; k < NC; ++k) {
+    long long run = s_excl[k] + incl[k] - tsum[k];
+    for (int q = 0; q < w; ++q) run += s_w[q][k];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      so[4 * P + j] = (int)spos[j];
-      woff[lb + 4 * P + j] = (int)wpos[j];
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      if (i0 + q < n) o.out[k][i0 + q] = (int)run;
+      run += v[q][k];
     }
   }
-  if (dead) return;
-  if (wb > wcap || sb > scap) {
-    if (lane == 0) {
+}
+
+// k_classify_fill: one warp per parent (grid-stride, no look-back): the
+// offsets come from the scan, the compacted lists from the stored masks
+// (ascending candidate order, as before).
+__global__ void __launch_bounds__(256)
+k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx,
+                const int* __restrict__ so, int* sidx, long long scap, const int* __restrict__ woff,
+                int* widx, int* wtgt, long long wcap, long long P0, long long P1, long long tb,
+                long long te, const unsigned* __restrict__ masks, long long mplane,
+                DevStatus* st) {
+  pdl_enter();
+  if (lists_overflowed(st)) return;
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(l);
+  const unsigned below = (1u << lane) - 1u;
+  if (woff[lb + 4 * P1] > wcap || so[4 * P1] > scap) {   // level totals past capacity
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       atomicOr(&st->flags, ST_OVERFLOW);
       atomicOr(&st->overflow_where, 1);
     }
     return;
   }
-  const unsigned below = (1u << lane) - 1u;
-  const int a0 = ps_off[P];
-  const int ncand = 4 * (ps_off[P + 1] - a0);
-  const long long mw = cl_wbase(ps_off, P, P0);
-  bool own[4];
-  unsigned ownm = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    own[j] = 4 * P + j >= tb && 4 * P + j < te;
-    ownm |= (unsigned)own[j] << j;
-  }
-  for (int c0 = 0; c0 < ncand; c0 += 32) {
-    const int c = c0 + lane;
-    const bool valid = c < ncand;
-    const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    const unsigned mine =
-        lane < 4 && ((ownm >> lane) & 1) ? masks[lane * mplane + mw + (c0 >> 5)] : 0u;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long P = P0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); P < P1;
+       P += nwarps) {
+    long long wpos[4], spos[4];
+    const int wl = lane < 4 ? woff[lb + 4 * P + lane] : 0;
+    const int sl = lane < 4 ? so[4 * P + lane] : 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (!own[j]) continue;
-      const unsigned m = __shfl_sync(0xffffffffu, mine, j);
-      const unsigned sm = vm & ~m;
-      if ((m >> lane) & 1u) {
-        const long long o = wpos[j] + __popc(m & below);
-        widx[o] = (int)(lb + cand);
-        wtgt[o] = (int)(lb + 4 * P + j);
+      wpos[j] = __shfl_sync(0xffffffffu, wl, j);
+      spos[j] = __shfl_sync(0xffffffffu, sl, j);
+    }
+    const int a0 = ps_off[P];
+    const int ncand = 4 * (ps_off[P + 1] - a0);
+    const long long mw = cl_wbase(ps_off, P, P0);
+    bool own[4];
+    unsigned ownm = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      own[j] = 4 * P + j >= tb && 4 * P + j < te;
+      ownm |= (unsigned)own[j] << j;
+    }
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+      const int c = c0 + lane;
+      const bool valid = c < ncand;
+      const int cand = valid ? 4 * ps_idx[a0 + (c >> 2)] + (c & 3) : 0;
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      const unsigned mine =
+          lane < 4 && ((ownm >> lane) & 1) ? masks[lane * mplane + mw + (c0 >> 5)] : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!own[j]) continue;
+        const unsigned m = __shfl_sync(0xffffffffu, mine, j);
+        const unsigned sm = vm & ~m;
+        if ((m >> lane) & 1u) {
+          const long long q = wpos[j] + __popc(m & below);
+          widx[q] = (int)(lb + cand);
+          wtgt[q] = (int)(lb + 4 * P + j);
+        }
+        if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
+        wpos[j] += __popc(m);
+        spos[j] += __popc(sm);
       }
-      if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
-      wpos[j] += __popc(m);
-      spos[j] += __popc(sm);
     }
   }
 }
@@ -592,86 +622,44 @@ k_reclassify_pred(int L, LevelGeo geo, double theta, const int* __restrict__ s_o
   }
 }
 
-__global__ void __launch_bounds__(CL_WARPS * 32)
-k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx, int* o_p2p,
-                  int* i_p2p, long long cap_p2p, int* o_p2l, int* i_p2l, long long cap_p2l,
-                  int* o_m2p, int* i_m2p, long long cap_m2p, LookbackState lbs, unsigned ntiles,
-                  long long tb, long long te, const int4* __restrict__ cnt,
-                  const unsigned* __restrict__ masks, long long mplane, DevStatus* st) {
+__global__ void __launch_bounds__(256)
+k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx,
+                  const int* __restrict__ o_p2p, int* i_p2p, long long cap_p2p,
+                  const int* __restrict__ o_p2l, int* i_p2l, long long cap_p2l,
+                  const int* __restrict__ o_m2p, int* i_m2p, long long cap_m2p, long long tb,
+                  long long te, const unsigned* __restrict__ masks, long long mplane,
+                  DevStatus* st) {
   pdl_enter();
-  __shared__ int s_cnt[CL_WARPS][CL_TPW][3];
-  __shared__ long long s_excl[3];
-  __shared__ unsigned s_tile;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
-  __syncthreads();
-  const unsigned tile = s_tile;
-  const bool dead = lists_overflowed(st);
-  const long long bw = tb + ((long long)tile * CL_WARPS + w) * CL_TPW;
-  if (lane < CL_TPW) {
-    int4 c = make_int4(0, 0, 0, 0);
-    if (bw + lane < te && !dead) c = cnt[bw + lane - tb];
-    s_cnt[w][lane][0] = c.x;
-    s_cnt[w][lane][1] = c.y;
-    s_cnt[w][lane][2] = c.z;
-  }
-  __syncthreads();
-  if (w == 0) {
-    long long agg[3] = {0, 0, 0}, excl[3];
-    for (int q = 0; q < CL_WARPS * CL_TPW; ++q)
-      for (int k = 0; k < 3; ++k) agg[k] += (&s_cnt[0][0][0])[3 * q + k];
-    lb_prefix<3>(lbs, tile, agg, excl);
-    if (lane == 0)
-      for (int k = 0; k < 3; ++k) s_excl[k] = excl[k];
-  }
-  __syncthreads();
-  long long pos[3] = {s_excl[0], s_excl[1], s_excl[2]};
-  for (int q = 0; q < w; ++q)
-    for (int u = 0; u < CL_TPW; ++u)
-      for (int k = 0; k < 3; ++k) pos[k] += s_cnt[q][u][k];
-  if (tile == ntiles - 1 && w == CL_WARPS - 1 && lane == 0) {
-    long long tot[3] = {pos[0], pos[1], pos[2]};
-    for (int u = 0; u < CL_TPW; ++u)
-      for (int k = 0; k < 3; ++k) tot[k] += s_cnt[w][u][k];
-    o_p2p[te] = (int)tot[0];
-    o_p2l[te] = (int)tot[1];
-    o_m2p[te] = (int)tot[2];
-  }
-  const unsigned below = (1u << lane) - 1u;
-  for (int u = 0; u < CL_TPW; ++u) {
-    const long long b = bw + u;
-    if (b >= te) break;
-    if (lane == 0) {
-      o_p2p[b] = (int)pos[0];
-      o_p2l[b] = (int)pos[1];
-      o_m2p[b] = (int)pos[2];
-    }
-    const int n0 = s_cnt[w][u][0], n1 = s_cnt[w][u][1], n2 = s_cnt[w][u][2];
-    if (!dead && pos[0] + n0 <= cap_p2p && pos[1] + n1 <= cap_p2l && pos[2] + n2 <= cap_m2p) {
-      const int a0 = s_off[b], a1 = s_off[b + 1];
-      const long long wb = (b - tb) + (a0 - s_off[tb]) / 32;
-      long long q0 = pos[0], q1 = pos[1], q2 = pos[2];
-      for (int c0 = a0; c0 < a1; c0 += 32) {
-        const int c = c0 + lane;
-        const int ch = (c0 - a0) >> 5;
-        const int src = c < a1 ? s_idx[c] : 0;
-        const unsigned vm = __ballot_sync(0xffffffffu, c < a1);
-        const unsigned ml = masks[wb + ch], mm = masks[mplane + wb + ch];
-        const unsigned mp = vm & ~(ml | mm);
-        if ((mp >> lane) & 1u) i_p2p[q0 + __popc(mp & below)] = src;
-        if ((ml >> lane) & 1u) i_p2l[q1 + __popc(ml & below)] = src;
-        if ((mm >> lane) & 1u) i_m2p[q2 + __popc(mm & below)] = src;
-        q0 += __popc(mp);
-        q1 += __popc(ml);
-        q2 += __popc(mm);
-      }
-    } else if (!dead && lane == 0) {
+  if (lists_overflowed(st)) return;
+  if (o_p2p[te] > cap_p2p || o_p2l[te] > cap_p2l || o_m2p[te] > cap_m2p) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
       atomicOr(&st->flags, ST_OVERFLOW);
       atomicOr(&st->overflow_where, 2);
     }
-    pos[0] += n0;
-    pos[1] += n1;
-    pos[2] += n2;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long b = tb + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5); b < te;
+       b += nwarps) {
+    long long q0 = o_p2p[b], q1 = o_p2l[b], q2 = o_m2p[b];
+    const int a0 = s_off[b], a1 = s_off[b + 1];
+    const long long wb = (b - tb) + (a0 - s_off[tb]) / 32;
+    for (int c0 = a0; c0 < a1; c0 += 32) {
+      const int c = c0 + lane;
+      const int ch = (c0 - a0) >> 5;
+      const int src = c < a1 ? s_idx[c] : 0;
+      const unsigned vm = __ballot_sync(0xffffffffu, c < a1);
+      const unsigned ml = masks[wb + ch], mm = masks[mplane + wb + ch];
+      const unsigned mp = vm & ~(ml | mm);
+      if ((mp >> lane) & 1u) i_p2p[q0 + __popc(mp & below)] = src;
+      if ((ml >> lane) & 1u) i_p2l[q1 + __popc(ml & below)] = src;
+      if ((mm >> lane) & 1u) i_m2p[q2 + __popc(mm & below)] = src;
+      q0 += __popc(mp);
+      q1 += __popc(ml);
+      q2 += __popc(mm);
+    }
   }
 }
 
@@ -798,17 +786,25 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const long long tb = part.lo(l), te = part.hi(l);
     const long long P0 = tb >> 2, P1 = (te + 3) >> 2;
     if (cl_split() && P1 - P0 >= CL_SPLIT_MIN) {
-      const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS - 1) / CL_WARPS);
+      const long long nt = 4 * (P1 - P0);
+      const unsigned stiles = (unsigned)((nt + SCAN_TILE - 1) / SCAN_TILE);
+      const unsigned wgrid = std::min(nblk((P1 - P0) * 32, 256), 8u * 148u);
       note_launch();
-      launch(k_classify_pred, std::min(nblk((P1 - P0) * 32, 256), 8u * 148u), 256, 0, st, l, geo,
-             theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), P0, P1, tb, te,
-             Ls.cl_cnt.as<int2>(), Ls.cl_mask.as<unsigned>(), mplane, dstat);
-      note_launch();
-      launch(k_classify_fill, ntiles, CL_WARPS * 32, 0, st, l, Ls.s_off[cur].as<int>(),
-             Ls.s_idx[cur].as<int>(), Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(),
-             Ls.cap_strong, woff, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak,
-             lbstate(), ntiles, P0, P1, tb, te, Ls.cl_cnt.as<int2>(),
+      launch(k_classify_pred, wgrid, 256, 0, st, l, geo, theta, Ls.s_off[cur].as<int>(),
+             Ls.s_idx[cur].as<int>(), P0, P1, tb, te, Ls.cl_cnt.as<int2>(),
              Ls.cl_mask.as<unsigned>(), mplane, dstat);
+      const ScanOut so{{woff + level_base(l) + 4 * P0, Ls.s_off[1 - cur].as<int>() + 4 * P0,
+                        nullptr},
+                       woff + level_base(l), woff + level_base(l + 1)};
+      note_launch();
+      launch(k_scan_counts<2, 2>, stiles, SCAN_THREADS, 0, st,
+             reinterpret_cast<const int*>(Ls.cl_cnt.as<int2>()), nt, so, lbstate(), stiles,
+             dstat);
+      note_launch();
+      launch(k_classify_fill, wgrid, 256, 0, st, l, Ls.s_off[cur].as<int>(),
+             Ls.s_idx[cur].as<int>(), Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(),
+             Ls.cap_strong, woff, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, P0,
+             P1, tb, te, Ls.cl_mask.as<unsigned>(), mplane, dstat);
     } else {
       const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
       note_launch();
@@ -824,16 +820,24 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const long long tb = part.lo(L), te = part.hi(L);
     const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
     if (cl_split() && te - tb >= 4 * CL_SPLIT_MIN) {
+      const unsigned stiles = (unsigned)((te - tb + SCAN_TILE - 1) / SCAN_TILE);
+      const unsigned wgrid = std::min(nblk((te - tb) * 32, 256), 8u * 148u);
       note_launch();
-      launch(k_reclassify_pred, std::min(nblk((te - tb) * 32, 256), 8u * 148u), 256, 0, st, L,
-             geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(), tb, te,
-             Ls.cl_cnt.as<int4>(), Ls.cl_mask.as<unsigned>(), rplane, dstat);
+      launch(k_reclassify_pred, wgrid, 256, 0, st, L, geo, theta, Ls.s_off[cur].as<int>(),
+             Ls.s_idx[cur].as<int>(), tb, te, Ls.cl_cnt.as<int4>(), Ls.cl_mask.as<unsigned>(),
+             rplane, dstat);
+      const ScanOut so{{Ls.p2p_off.as<int>() + tb, Ls.p2l_off.as<int>() + tb,
+                        Ls.m2p_off.as<int>() + tb},
+                       nullptr, nullptr};
       note_launch();
-      launch(k_reclassify_fill, ntiles, CL_WARPS * 32, 0, st, Ls.s_off[cur].as<int>(),
+      launch(k_scan_counts<3, 4>, stiles, SCAN_THREADS, 0, st,
+             reinterpret_cast<const int*>(Ls.cl_cnt.as<int4>()), te - tb, so, lbstate(), stiles,
+             dstat);
+      note_launch();
+      launch(k_reclassify_fill, wgrid, 256, 0, st, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), Ls.cap_p2p,
              Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), Ls.cap_p2l, Ls.m2p_off.as<int>(),
-             Ls.m2p_idx.as<int>(), Ls.cap_m2p, lbstate(), ntiles, tb, te, Ls.cl_cnt.as<int4>(),
-             Ls.cl_mask.as<unsigned>(), rplane, dstat);
+             Ls.m2p_idx.as<int>(), Ls.cap_m2p, tb, te, Ls.cl_mask.as<unsigned>(), rplane, dstat);
     } else {
       note_launch();
       launch(k_reclassify, ntiles, CL_WARPS * 32, 0, st,
