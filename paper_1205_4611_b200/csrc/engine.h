@@ -101,7 +101,26 @@ struct TreeState {
   const double* g_p = nullptr;       //   device memory), original order
   const double2* epos_p = nullptr;
   cudaEvent_t inputs_ready = nullptr;  // strengths / evaluation points uploaded (host calls)
-  DBuf keys_in, keys_out, vals_in, vals_out, cub_tmp;
+  DBuf keys_in, keys_out, vals_in, vals_out, cub_tmp, cub_tmp2;
+  // second stream for the y-axis rank sort (runs beside the x-axis sort)
+  struct Aux {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    void ensure() {
+      if (s) return;
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    }
+    Aux() = default;
+    Aux(const Aux&) = delete;
+    Aux& operator=(const Aux&) = delete;
+    ~Aux() {
+      if (s) cudaStreamDestroy(s);
+      if (fork) cudaEventDestroy(fork);
+      if (join) cudaEventDestroy(join);
+    }
+  } aux;
   DBuf perm_x, perm_y, rank_x, rank_y;
   DBuf X0, X1, Y0, Y1;               // int2 (rank_x, rank_y) arrays
   DBuf xpar0, xpar1, ypar0, ypar1, cutrank;

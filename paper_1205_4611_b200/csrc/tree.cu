@@ -34,6 +34,12 @@ constexpr int PART_THREADS = 256;
 #ifndef TREE_SUB_THREADS
 #define TREE_SUB_THREADS 512
 #endif
+#ifndef TREE_FORK_SORT
+#define TREE_FORK_SORT 1   // y-axis rank sort on a side stream
+#endif
+#ifndef TREE_FORK_MIN
+#define TREE_FORK_MIN 4096
+#endif
 #ifndef TREE_SMEM_BUDGET
 #define TREE_SMEM_BUDGET (110 * 1024)
 #endif
@@ -833,12 +839,27 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         int nb = 0;
         while ((1ll << nb) < n) ++nb;
         const int key_bits = std::min(32, std::max(16, (nb + 4 + 7) / 8 * 8));
+        const bool fork = TREE_FORK_SORT && n >= TREE_FORK_MIN;
         if (axis == 0) {
           note_launch();
           launch(k_make_keys32, nblk(n, 256), 256, 0, st, pos, n, T.rect_tab.as<Rect>(), kin,
                  T.vals_in.as<int>(), 32 - key_bits);
+          if (fork) {
+            // the y-axis sort runs on the side stream while x sorts and fixes ties
+            T.aux.ensure();
+            FMM_CUDA(cudaEventRecord(T.aux.fork, st));
+            FMM_CUDA(cudaStreamWaitEvent(T.aux.s, T.aux.fork, 0));
+            radix_sort_pairs(T.cub_tmp2, kin + n, kout + n, T.vals_in.as<int>(),
+                             T.perm_y.as<int>(), n, key_bits, T.aux.s);
+            FMM_CUDA(cudaEventRecord(T.aux.join, T.aux.s));
+          }
         }
-        radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, key_bits, st);
+        if (fork) {
+          kout += axis * n;
+          if (axis == 1) FMM_CUDA(cudaStreamWaitEvent(st, T.aux.join, 0));
+        }
+        if (!fork || axis == 0)
+          radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, key_bits, st);
         note_launch();
         RankOut o{T.rank_x.as<int>(), nullptr, nullptr, nullptr, nullptr, nullptr};
         if (axis == 1)
