@@ -59,6 +59,7 @@ struct fmm2d_ctx {
   DevStatus* h_status = nullptr;
   int* h_hist = nullptr;
   cudaEvent_t ev[10] = {};
+  cudaEvent_t ev_side[3] = {};      // P2M / M2M on the tree's side stream (overlapped)
   std::string err;
   bool have_tree = false, have_lists = false, have_eval = false;
   double theta = 0.5;

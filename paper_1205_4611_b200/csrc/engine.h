@@ -204,8 +204,9 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
                       cudaStream_t st, const Part& part = Part());
 
 void compute_radius(TreeState& T, cudaStream_t st);
+// which: 0 = P2M and P2L, 1 = P2M only (needs the tree only), 2 = P2L only (needs lists)
 void run_upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                DevStatus* dstat, cudaStream_t st, const Part& part = Part());
+                DevStatus* dstat, cudaStream_t st, const Part& part = Part(), int which = 0);
 // M2M for parent levels lmax..lmin (descending); lmax < 0 means L-1
 void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part = Part(),
              int lmin = 1, int lmax = -1);

@@ -754,14 +754,17 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 template <int PM>
 struct Launch {
   static void upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                     DevStatus* dstat, cudaStream_t st, const Part& part) {
+                     DevStatus* dstat, cudaStream_t st, const Part& part, int which) {
     const int L = T.L, p = E.p;
     if (L == 0) return;
     const long long b0 = part.lo(L), b1 = part.hi(L);
-    note_launch();
-    launch(k_p2m<PM>, nblk(b1 - b0, 128), 128, 0, st, L, b0, b1, offL, T.src_pos.as<double2>(),
-                                                  T.src_g.as<double>(), T.box_cx.as<double>(),
-                                                  T.box_cy.as<double>(), E.mult.as<double2>(), p);
+    if (which != 2) {
+      note_launch();
+      launch(k_p2m<PM>, nblk(b1 - b0, 128), 128, 0, st, L, b0, b1, offL, T.src_pos.as<double2>(),
+             T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
+             E.mult.as<double2>(), p);
+    }
+    if (which == 1) return;
     note_launch();
     E.p2l_rows.reserve(sizeof(double2) * std::max(1ll, Ls.cap_p2l) * (p + 1));
     launch(k_p2l_pair<PM>, 8 * sm_count(), 128, 0, st, 
@@ -861,9 +864,9 @@ void dispatch_p(int p, F&& f) {
 bool p_supported(int p) { return p >= 1 && p <= 64; }
 
 void run_upward(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
-                DevStatus* dstat, cudaStream_t st, const Part& part) {
+                DevStatus* dstat, cudaStream_t st, const Part& part, int which) {
   dispatch_p(E.p, [&](auto pm) {
-    Launch<decltype(pm)::value>::upward(T, Ls, E, offL, dstat, st, part);
+    Launch<decltype(pm)::value>::upward(T, Ls, E, offL, dstat, st, part, which);
   });
 }
 void run_m2m(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part, int lmin,
