@@ -203,11 +203,21 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     // P2P adds into phi and scatters to input order (engine.py:263-267)
     run_p2p(T, Ls, E, offL, values, dst, c->st);
     FMM_CUDA(cudaEventRecord(c->ev[8], c->st));
+    // the result download starts now, on the copy stream beside the report
+    // kernels, instead of after the status round trip (a retry below simply
+    // rewrites the output; an error leaves it unspecified)
+    if (!device_io && out) {
+      FMM_CUDA(cudaStreamWaitEvent(c->st_copy, c->ev[8], 0));
+      FMM_CUDA(cudaMemcpyAsync(out, values, sizeof(double2) * T.m, cudaMemcpyDeviceToHost,
+                               c->st_copy));
+      FMM_CUDA(cudaEventRecord(c->ev[9], c->st_copy));
+    }
     run_stats(T, Ls, dst, c->st);
     fetch_status(c);
     FMM_CUDA(cudaMemcpyAsync(c->h_hist, Ls.hist.p, sizeof(int) * 4 * HIST_BINS,
                              cudaMemcpyDeviceToHost, c->st));
     FMM_CUDA(cudaStreamSynchronize(c->st));
+    if (!device_io && out) FMM_CUDA(cudaStreamSynchronize(c->st_copy));
     FMM_CUDA(cudaGetLastError());
     const DevStatus& s = *c->h_status;
     if (s.flags & ST_RANK_RETRY) {    // rare: clustered ties beyond the 32-bit keys
@@ -248,12 +258,7 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     throw ApiError{FMM2D_ESINGULAR, "m2l shift must be nonzero (boxes are separated)"};
   if (s.flags & ST_M2P_SINGULAR)
     throw ApiError{FMM2D_ESINGULAR, "m2p target coincides with the expansion center"};
-  if (!device_io && out) {
-    FMM_CUDA(cudaMemcpyAsync(out, values, sizeof(double2) * T.m, cudaMemcpyDeviceToHost, c->st));
-    FMM_CUDA(cudaEventRecord(c->ev[9], c->st));
-    FMM_CUDA(cudaStreamSynchronize(c->st));
-    r.d2h_bytes = sizeof(double2) * T.m;
-  }
+  if (!device_io && out) r.d2h_bytes = sizeof(double2) * T.m;   // downloaded above
   // report
   for (int q = 0; q < 8; ++q) r.phase_ms[q] = ev_ms(c->ev[q], c->ev[q + 1]);
   if (UPWARD_OVERLAP && L > 0) {

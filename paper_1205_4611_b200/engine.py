@@ -53,7 +53,8 @@ def _histograms(ctx: _lib.Context, rep: _lib.Report) -> dict[str, dict[int, int]
         nb = int(rep.max_len[k]) + 1
         h = np.zeros(nb, np.int64)
         ctx.check(ctx.lib.fmm2d_histogram(ctx.h, k, _lib.iptr(h), nb))
-        out[name] = {int(i): int(c) for i, c in enumerate(h) if c}
+        nz = np.flatnonzero(h)
+        out[name] = dict(zip(nz.tolist(), h[nz].tolist()))
     return out
 
 
