@@ -51,6 +51,7 @@ struct fmm2d_ctx {
   cudaStream_t own_st = nullptr;     // the stream this context created (st may be external)
   cudaStream_t st_copy = nullptr;    // H2D of the inputs needed late (strengths, evaluation points)
   cudaEvent_t ev_inputs = nullptr;
+  cudaEvent_t ev_pos = nullptr;      // positions uploaded (the late inputs queue behind)
   TreePlan plan;
   TreeState T;
   ListState Ls;

@@ -93,6 +93,10 @@ void set_inputs(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, int
   T.pos.reserve(sizeof(double2) * n);
   T.g.reserve(sizeof(double) * n);
   FMM_CUDA(cudaMemcpyAsync(T.pos.p, pos, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
+  // the late inputs queue behind the positions: the positions get the whole
+  // host link (the tree waits on them), the rest lands during the rank sorts
+  FMM_CUDA(cudaEventRecord(c->ev_pos, c->st));
+  FMM_CUDA(cudaStreamWaitEvent(c->st_copy, c->ev_pos, 0));
   FMM_CUDA(cudaMemcpyAsync(T.g.p, g, sizeof(double) * n, cudaMemcpyHostToDevice, c->st_copy));
   *h2d += (sizeof(double2) + sizeof(double)) * n;
   T.pos_p = T.pos.as<double2>();
@@ -311,6 +315,7 @@ int fmm2d_create(fmm2d_ctx** out, int device) {
     c->own_st = c->st;
     FMM_CUDA(cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_inputs, cudaEventDisableTiming));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_pos, cudaEventDisableTiming));
     for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
     for (auto& e : c->ev_side) FMM_CUDA(cudaEventCreate(&e));
     c->d_status.reserve(sizeof(DevStatus));
@@ -342,6 +347,7 @@ void fmm2d_destroy(fmm2d_ctx* c) {
   if (c->h_hist) cudaFreeHost(c->h_hist);
   if (c->st_copy) cudaStreamSynchronize(c->st_copy);
   if (c->ev_inputs) cudaEventDestroy(c->ev_inputs);
+  if (c->ev_pos) cudaEventDestroy(c->ev_pos);
   if (c->st_copy) cudaStreamDestroy(c->st_copy);
   if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;

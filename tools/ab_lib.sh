@@ -11,6 +11,6 @@ for cfg in $CFGS; do
     else
       FMM2D_LIBRARY=build/ab/libfmm2d_$v.so timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline > $f 2>&1
     fi
-    echo "$cfg $v $(python -c "import json;d=json.loads(open('$f').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4),d['phase_ms'])" 2>&1 | tail -1)"
+    echo "$cfg $v $(python -c "import json;d=json.loads(open('$f').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4),'e2e',round(d['e2e']['ms_per_step'],4),d['phase_ms'])" 2>&1 | tail -1)"
   done
 done
