@@ -29,10 +29,13 @@ namespace {
 
 constexpr int PART_THREADS = 256;
 #ifndef TREE_PART_ITEMS
-#define TREE_PART_ITEMS 8
+#define TREE_PART_ITEMS 4
 #endif
 #ifndef TREE_SUB_THREADS
 #define TREE_SUB_THREADS 512
+#endif
+#ifndef TREE_KEY_EXTRA
+#define TREE_KEY_EXTRA 4   // rank key bits beyond log2 N (rounded up to a radix digit)
 #endif
 #ifndef TREE_FORK_SORT
 #define TREE_FORK_SORT 1   // y-axis rank sort on a side stream
@@ -838,7 +841,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         // for small N, equal-key runs stay short (k_fix_ties orders them exactly)
         int nb = 0;
         while ((1ll << nb) < n) ++nb;
-        const int key_bits = std::min(32, std::max(16, (nb + 4 + 7) / 8 * 8));
+        const int key_bits = std::min(32, std::max(16, (nb + TREE_KEY_EXTRA + 7) / 8 * 8));
         const bool fork = TREE_FORK_SORT && n >= TREE_FORK_MIN;
         if (axis == 0) {
           note_launch();
