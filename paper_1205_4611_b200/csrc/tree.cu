@@ -37,6 +37,9 @@ constexpr int PART_THREADS = 256;
 #ifndef TREE_KEY_EXTRA
 #define TREE_KEY_EXTRA 4   // rank key bits beyond log2 N (rounded up to a radix digit)
 #endif
+#ifndef TREE_FUSE_RECORDS_MAX
+#define TREE_FUSE_RECORDS_MAX (1ll << 22)
+#endif
 #ifndef TREE_FORK_SORT
 #define TREE_FORK_SORT 1   // y-axis rank sort on a side stream
 #endif
@@ -826,6 +829,11 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     for (DBuf* b : {&T.X0, &T.X1, &T.Y0, &T.Y1}) b->reserve(sizeof(int2) * n);
     const long long pmax = (1ll << std::max(sb, 1)) + 2;
     for (DBuf* b : {&T.xpar0, &T.xpar1, &T.ypar0, &T.ypar1}) b->reserve(pmax);
+    // small N: the y tie pass scatters the split records itself (all arrays
+    // L2-resident); large N: rank arrays + one gather pass (k_init_arrays),
+    // whose random reads hit a 4-byte rank array instead of scattering 8-byte
+    // records across a DRAM-sized copy
+    const bool fuse_records = n <= TREE_FUSE_RECORDS_MAX;
     for (int axis = 0; axis < 2; ++axis) {
       int* perm = axis ? T.perm_y.as<int>() : T.perm_x.as<int>();
       if (T.exact_keys) {
@@ -864,8 +872,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
         if (!fork || axis == 0)
           radix_sort_pairs(T.cub_tmp, kin, kout, T.vals_in.as<int>(), perm, n, key_bits, st);
         note_launch();
-        RankOut o{T.rank_x.as<int>(), nullptr, nullptr, nullptr, nullptr, nullptr};
-        if (axis == 1)
+        RankOut o{axis ? T.rank_y.as<int>() : T.rank_x.as<int>(), nullptr, nullptr, nullptr,
+                  nullptr, nullptr};
+        if (axis == 1 && fuse_records)
           o = RankOut{nullptr, T.rank_x.as<int>(), T.X0.as<int2>(), T.Y0.as<int2>(),
                       T.xpar0.as<unsigned char>(), T.ypar0.as<unsigned char>()};
         launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, o, dstat);
@@ -874,7 +883,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       note_launch();
       launch(k_rank_scatter, nblk(n, 256), 256, 0, st, n, perm, axis ? T.rank_y.as<int>() : T.rank_x.as<int>());
     }
-    if (T.exact_keys) {
+    if (T.exact_keys || !fuse_records) {
       note_launch();
       launch(k_init_arrays, nblk(n, 256), 256, 0, st, n, T.perm_x.as<int>(), T.perm_y.as<int>(),
              T.rank_x.as<int>(), T.rank_y.as<int>(), T.X0.as<int2>(), T.Y0.as<int2>(),
