@@ -83,6 +83,31 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
   by = fma(gs, dy, by);
 }
 
+// sum of the staged sources [j0, j1) on target y into (ax, ay): 4-way
+// unrolled, two accumulator pairs, fixed order
+__device__ __forceinline__ void p2p_slice(const double2* sp, const double* sg, int j0, int j1,
+                                          double2 y, double& ax, double& ay, int& skips) {
+  const double2* zp = sp + j0;
+  const double* gp = sg + j0;
+  const int n = j1 - j0;
+  double bx0 = 0.0, by0 = 0.0, bx1 = 0.0, by1 = 0.0;
+  int j = 0;
+  for (; j + 4 <= n; j += 4) {
+    const double2 z0 = zp[j], z1 = zp[j + 1], z2 = zp[j + 2], z3 = zp[j + 3];
+    const double g0 = gp[j], g1 = gp[j + 1], g2 = gp[j + 2], g3 = gp[j + 3];
+    p2p_term(z0.x, z0.y, g0, y.x, y.y, bx0, by0, skips);
+    p2p_term(z1.x, z1.y, g1, y.x, y.y, bx1, by1, skips);
+    p2p_term(z2.x, z2.y, g2, y.x, y.y, bx0, by0, skips);
+    p2p_term(z3.x, z3.y, g3, y.x, y.y, bx1, by1, skips);
+  }
+  for (; j < n; ++j) {
+    const double2 z = zp[j];
+    p2p_term(z.x, z.y, gp[j], y.x, y.y, bx0, by0, skips);
+  }
+  ax += bx0 + bx1;
+  ay += by0 + by1;
+}
+
 // One warp per target leaf.  The leaf's near sources (the concatenated source
 // ranges of its p2p boxes, ascending) are staged into a per-warp SMEM buffer
 // with cp.async; the box table (ids, ranges) is fetched once per 32 boxes
@@ -93,6 +118,7 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
 // CONTIGUOUS slice of the staged sources (immediate-offset SMEM reads,
 // 4-way unrolled, two accumulator pairs), then the G partial sums are folded
 // in fixed lane order -- deterministic, no atomics on values.
+template <bool DUAL>
 __global__ void __launch_bounds__(P2P_THREADS)
 k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __restrict__ eoff,
       const int* __restrict__ n_off, const int* __restrict__ n_idx,
@@ -111,7 +137,16 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
   double2* sp = s_pos[w];
   double* sg = s_g[w];
   int skips = 0;
-  for (int eb = e0; eb < e1; eb += 32) {
+  // DUAL: up to 64 points per pass -- block A (<= 32 points, G lane groups)
+  // and, for leaves of 33..64 points, block B (the rest, GB groups) share
+  // every staged chunk, so the near sources are staged once per 64 points
+  for (int eb = e0; eb < e1; eb += DUAL ? 64 : 32) {
+    const int neB = DUAL ? max(0, min(32, e1 - eb - 32)) : 0;
+    const int GB = neB ? 32 / neB : 1;
+    const bool activeB = neB && lane < GB * neB;
+    const int eiB = neB ? lane % neB : 0, grpB = activeB ? lane / neB : 0;
+    const double2 yB = activeB ? eval_pos[eb + 32 + eiB] : make_double2(0.0, 0.0);
+    double axB = 0.0, ayB = 0.0;
     const int ne = min(32, e1 - eb);
     const int G = 32 / ne;
     const bool active = lane < G * ne;
@@ -204,28 +239,10 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
 #endif
       cp_async_wait_all();
       __syncwarp();
-      if (active) {
-        const int j0 = fill * grp / G, j1 = fill * (grp + 1) / G;
-        const double2* zp = sp + j0;
-        const double* gp = sg + j0;
-        const int n = j1 - j0;
-        double bx0 = 0.0, by0 = 0.0, bx1 = 0.0, by1 = 0.0;
-        int j = 0;
-        for (; j + 4 <= n; j += 4) {
-          const double2 z0 = zp[j], z1 = zp[j + 1], z2 = zp[j + 2], z3 = zp[j + 3];
-          const double g0 = gp[j], g1 = gp[j + 1], g2 = gp[j + 2], g3 = gp[j + 3];
-          p2p_term(z0.x, z0.y, g0, y.x, y.y, bx0, by0, skips);
-          p2p_term(z1.x, z1.y, g1, y.x, y.y, bx1, by1, skips);
-          p2p_term(z2.x, z2.y, g2, y.x, y.y, bx0, by0, skips);
-          p2p_term(z3.x, z3.y, g3, y.x, y.y, bx1, by1, skips);
-        }
-        for (; j < n; ++j) {
-          const double2 z = zp[j];
-          p2p_term(z.x, z.y, gp[j], y.x, y.y, bx0, by0, skips);
-        }
-        ax += bx0 + bx1;
-        ay += by0 + by1;
-      }
+      if (active) p2p_slice(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
+      // second block of points (leaves of 33..64 points): same staged chunk
+      if (DUAL && activeB)
+        p2p_slice(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
       __syncwarp();
     }
     // fold the G lane groups of every point in fixed order
@@ -239,6 +256,19 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
       const double2 f = phi_in ? phi_in[e] : make_double2(0.0, 0.0);
       // input order (engine.py:266-267), or tree order for distributed ranks
       values[eval_perm ? (long long)eval_perm[e] : e - out_base] = make_double2(f.x + ax, f.y - ay);
+    }
+    if (DUAL && neB) {
+      for (int k = 1; k < GB; ++k) {
+        const double ox = __shfl_sync(0xffffffffu, axB, lane + k * neB);
+        const double oy = __shfl_sync(0xffffffffu, ayB, lane + k * neB);
+        if (grpB == 0) { axB += ox; ayB += oy; }
+      }
+      if (activeB && grpB == 0) {
+        const int e = eb + 32 + eiB;
+        const double2 f = phi_in ? phi_in[e] : make_double2(0.0, 0.0);
+        values[eval_perm ? (long long)eval_perm[e] : e - out_base] =
+            make_double2(f.x + axB, f.y - ayB);
+      }
     }
   }
   for (int d = 16; d; d >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, d);
@@ -288,11 +318,16 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part,
              long long out_base) {
   const long long b0 = part.lo(T.L), b1 = part.hi(T.L);
+  // leaves of more than 32 points (mean evaluation points per leaf): the
+  // two-block kernel stages each leaf's near sources once per 64 points; the
+  // one-block kernel keeps 64 registers for the common <= 32-point leaves
+  const long long nleaf = 1ll << (2 * T.L);
+  const bool dual = (T.m + nleaf - 1) / nleaf > 32;
   note_launch();
-  launch(k_p2p, nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0, st, 
-      b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), T.src_pos.as<double2>(),
-      T.src_g.as<double>(), T.epos_t, out_base >= 0 ? nullptr : T.eperm_t, E.phi.as<double2>(),
-      values, out_base, dstat);
+  launch(dual ? k_p2p<true> : k_p2p<false>, nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0,
+         st, b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(),
+         T.src_pos.as<double2>(), T.src_g.as<double>(), T.epos_t,
+         out_base >= 0 ? nullptr : T.eperm_t, E.phi.as<double2>(), values, out_base, dstat);
 }
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
