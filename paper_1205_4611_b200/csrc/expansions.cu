@@ -298,6 +298,9 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 // coefficient and segment, coalesced row updates).  Targets wholly inside
 // the item are updated in place (exclusive owner, no atomics); targets whose
 // pairs span items leave ordered partials for k_m2l_fixup.
+#ifndef M2L_GRID_WAVES
+#define M2L_GRID_WAVES 16  // grid = 16 waves of resident CTAs (tail balance)
+#endif
 constexpr int M2L_ITEM = 128;
 
 // Per-order table T[j][k-1] = C(j+k-1, k-1), j = 0..PM, k = 1..PM, rows of
@@ -809,8 +812,8 @@ struct Launch {
                                       Cfg::SMEM));
         attr = true;
       }
-      const unsigned grid = (unsigned)std::min<long long>(std::max(1ll, items),
-                                                          (long long)Cfg::MINB * sm_count());
+      const unsigned grid = (unsigned)std::min<long long>(
+          std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
       note_launch();
       launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st, 
           total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
