@@ -33,6 +33,9 @@ constexpr int CL_WARPS = 8;     // warps per CTA
 constexpr int CL_PPW = 1;       // classify: parents (4 sibling targets each) per warp
 constexpr int CL_TPW = 8;       // reclassify: finest targets per warp
 constexpr int CL_MAXM = 16;     // ballot masks cached per target (512 candidates)
+#ifndef CL_GRID_CAP
+#define CL_GRID_CAP (8u * 148u)   // predicate / fill grids (warp per parent, grid-stride)
+#endif
 #ifndef CL_SPLIT_MIN
 #define CL_SPLIT_MIN 1024       // parents per level from which the split classify runs
 #endif
@@ -788,7 +791,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     if (cl_split() && P1 - P0 >= CL_SPLIT_MIN) {
       const long long nt = 4 * (P1 - P0);
       const unsigned stiles = (unsigned)((nt + SCAN_TILE - 1) / SCAN_TILE);
-      const unsigned wgrid = std::min(nblk((P1 - P0) * 32, 256), 8u * 148u);
+      const unsigned wgrid = std::min(nblk((P1 - P0) * 32, 256), CL_GRID_CAP);
       note_launch();
       launch(k_classify_pred, wgrid, 256, 0, st, l, geo, theta, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), P0, P1, tb, te, Ls.cl_cnt.as<int2>(),
@@ -821,7 +824,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
     if (cl_split() && te - tb >= 4 * CL_SPLIT_MIN) {
       const unsigned stiles = (unsigned)((te - tb + SCAN_TILE - 1) / SCAN_TILE);
-      const unsigned wgrid = std::min(nblk((te - tb) * 32, 256), 8u * 148u);
+      const unsigned wgrid = std::min(nblk((te - tb) * 32, 256), CL_GRID_CAP);
       note_launch();
       launch(k_reclassify_pred, wgrid, 256, 0, st, L, geo, theta, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), tb, te, Ls.cl_cnt.as<int4>(), Ls.cl_mask.as<unsigned>(),
