@@ -101,6 +101,10 @@ CASES = [
     ("uniform", 2_000, 11, None, False, F.TreeConfig(35, 0.5, 1)),
     ("uniform", 45 * 2**8, 12, None, False, F.TreeConfig(45, 0.5, 17)),
     ("uniform", 700, 13, None, False, F.TreeConfig(1000, 0.5, 17)),   # zero levels
+    # many separate evaluation points per leaf: the two-block P2P kernel
+    # (> 32 points per leaf, several 64-point passes), uniform and clustered
+    ("uniform", 4_000, 14, 30_000, False, F.TreeConfig(35, 0.5, 17)),
+    ("uniform", 4_000, 15, 30_000, True, F.TreeConfig(35, 0.5, 17)),
 ]
 
 
