@@ -46,7 +46,10 @@ def test_comm_layer_gloo(tmp_path, world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,kind,n,p", [(2, "uniform", 20000, 17), (4, "normal", 30000, 20),
-                                            (8, "uniform", 40000, 20), (4, "layer", 25000, 12)])
+                                            (8, "uniform", 40000, 20), (4, "layer", 25000, 12),
+                                            # owned windows large enough for the split
+                                            # connectivity kernels (>= 1024 parents per rank)
+                                            (2, "uniform", 400000, 17)])
 def test_distributed_matches_single_gpu(tmp_path, world, kind, n, p):
     import paper_1205_4611_b200 as F
     out = tmp_path / "dist.npz"
