@@ -301,7 +301,10 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 #ifndef M2L_GRID_WAVES
 #define M2L_GRID_WAVES 16  // grid = 16 waves of resident CTAs (tail balance)
 #endif
-constexpr int M2L_ITEM = 128;
+#ifndef M2L_ITEM_PAIRS
+#define M2L_ITEM_PAIRS 64    // pairs (threads) per CTA item: small CTAs, cheap barriers
+#endif
+constexpr int M2L_ITEM = M2L_ITEM_PAIRS;
 
 // Per-order table T[j][k-1] = C(j+k-1, k-1), j = 0..PM, k = 1..PM, rows of
 // even stride so consecutive k pairs are one 16-byte uniform constant load;
@@ -333,11 +336,9 @@ struct M2LDenseCfg {
   static constexpr int R = 2 * (PM + 1);          // SMEM rows (re/im per coefficient)
   static constexpr int STR = M2L_ITEM + 1;        // odd row stride: conflict-free
   static constexpr int SMEM = R * STR * 8;
-#ifdef M2L_MINB
-  static constexpr int MINB = PM <= 20 ? M2L_MINB : (PM <= 24 ? 3 : 2);
-#else
-  static constexpr int MINB = PM <= 20 ? 4 : (PM <= 24 ? 3 : 2);
-#endif
+  // resident warps per SM the register budget allows (128 / 168 / 252 regs)
+  static constexpr int WARPS = PM <= 20 ? 16 : (PM <= 24 ? 12 : 8);
+  static constexpr int MINB = WARPS / (M2L_ITEM / 32);
 };
 
 // one coalesced row update of a target segment's sum (coefficient j, part comp)
