@@ -291,9 +291,9 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 // cascade (840 at p=20) but 42 independent accumulation chains instead of a
 // wavefront, and alpha is the only register-resident array.
 //
-// Work split: all levels in one persistent launch over the flat pair list
-// (one global CSR sorted by (target, source)).  A CTA takes 128 consecutive
-// pairs, one per thread; every thread parks its b row in SMEM, then the CTA
+// Work split: all levels in one launch over the flat pair list (one global
+// CSR sorted by (target, source)).  A CTA takes M2L_ITEM consecutive pairs,
+// one per thread; every thread parks its b row in SMEM, then the CTA
 // folds each target segment in ascending pair order (one task per
 // coefficient and segment, coalesced row updates).  Targets wholly inside
 // the item are updated in place (exclusive owner, no atomics); targets whose
