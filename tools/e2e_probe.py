@@ -11,7 +11,7 @@ h_g = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
 h_g[:] = rng.uniform(-1, 1, n)
 h_out = torch.empty(n, dtype=torch.complex128, pin_memory=True).numpy()
 ps = F.ParticleSet(h_pos, h_g)
-cfg = F.TreeConfig(20, 0.5, 35)
+cfg = F.TreeConfig(35, 0.5, 20)   # n_desired_per_box, theta, p_terms (C2)
 for _ in range(3):
     F.fmm_evaluate(ps, cfg, out=h_out)
 ts, dev, tot = [], [], []
