@@ -129,6 +129,54 @@ int fmm2d_direct(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* 
                  int64_t m, const double* eval_xy, double* out_xy);
 
 /* ---------------------------------------------------------------------------
+ * Unit operators (replace fmm2d.operators, operators.py:63-297) on the GPU.
+ * Batched, any order p; coefficient arrays are c128[rows, p+1] row-major.
+ * Singular inputs return FMM2D_ESINGULAR with the reference's message.
+ * --------------------------------------------------------------------------- */
+/* operators.py:63-75 p2m over nbox boxes of points off[b]..off[b+1] -> c128[nbox, p+1] */
+int fmm2d_op_p2m(fmm2d_ctx* ctx, int64_t nbox, const int64_t* off, const double* pos_xy,
+                 const double* gamma, const double* center_xy, int p, double* out_xy);
+/* operators.py:78-93 p2l, same layout */
+int fmm2d_op_p2l(fmm2d_ctx* ctx, int64_t nbox, const int64_t* off, const double* pos_xy,
+                 const double* gamma, const double* center_xy, int p, double* out_xy);
+/* operators.py:127-148 m2m in place; variant 0 = "scaled" (unscaled fallback
+ * outside [1e-12, 1e12]), 1 = "unscaled" */
+int fmm2d_op_m2m(fmm2d_ctx* ctx, int64_t rows, int p, double* coeffs_xy, const double* shift_xy,
+                 int variant);
+/* operators.py:171-186 l2l in place */
+int fmm2d_op_l2l(fmm2d_ctx* ctx, int64_t rows, int p, double* coeffs_xy, const double* shift_xy);
+/* operators.py:189-220 m2l -> out c128[rows, p+1] */
+int fmm2d_op_m2l(fmm2d_ctx* ctx, int64_t rows, int p, const double* coeffs_xy,
+                 const double* shift_xy, double* out_xy);
+/* operators.py:227-234 l2p / 237-255 m2p of one expansion at nt targets */
+int fmm2d_op_l2p(fmm2d_ctx* ctx, int p, const double* coeffs_xy, const double* center_xy,
+                 int64_t nt, const double* tgt_xy, double* out_xy);
+int fmm2d_op_m2p(fmm2d_ctx* ctx, int p, const double* coeffs_xy, const double* center_xy,
+                 int64_t nt, const double* tgt_xy, double* out_xy);
+/* operators.py:258-277 reciprocal_parts -> re, im f64[nt, ns] and the skip count */
+int fmm2d_op_reciprocal_parts(fmm2d_ctx* ctx, int64_t ns, const double* src_xy, int64_t nt,
+                              const double* tgt_xy, double* re, double* im, int64_t* n_skip);
+/* operators.py:280-292 kernel_block -> phi c128[nt] and the skip count */
+int fmm2d_op_kernel_block(fmm2d_ctx* ctx, int64_t ns, const double* src_xy, const double* gamma,
+                          int64_t nt, const double* tgt_xy, double* out_xy, int64_t* n_skip);
+
+/* connectivity.py:47-68 classify_level: level geometry (nbox = 4^l boxes),
+ * parent strong CSR (local ids of level l-1); writes weak and strong CSR
+ * (offsets [nbox+1]; index arrays sized 16 * parent_off[nbox/4]) */
+int fmm2d_classify_level(fmm2d_ctx* ctx, int64_t nbox, const double* center_xy,
+                         const double* half_width, const double* half_height,
+                         const int64_t* parent_off, const int64_t* parent_idx, double theta,
+                         int64_t* weak_off, int64_t* weak_idx, int64_t* strong_off,
+                         int64_t* strong_idx);
+/* connectivity.py:71-96 reclassify_finest: finest geometry + strong CSR ->
+ * p2p / p2l / m2p CSR (index arrays sized strong_off[nbox]) */
+int fmm2d_reclassify_finest(fmm2d_ctx* ctx, int64_t nbox, const double* center_xy,
+                            const double* half_width, const double* half_height,
+                            const int64_t* strong_off, const int64_t* strong_idx, double theta,
+                            int64_t* p2p_off, int64_t* p2p_idx, int64_t* p2l_off,
+                            int64_t* p2l_idx, int64_t* m2p_off, int64_t* m2p_idx);
+
+/* ---------------------------------------------------------------------------
  * Distributed evaluation (the reference is single-process,
  * SPEC.md:409).  One context per rank, one rank per GPU.  The library runs the
  * compute phases; the caller (paper_1205_4611_b200/distributed.py, through

@@ -19,6 +19,7 @@ CSRC = PKG / "csrc"
 OUT = PKG / "libfmm2d.so"
 OBJ = PKG / "_obj"
 SOURCES = ["scan.cu", "tree.cu", "connect.cu", "expansions.cu", "nearfield.cu", "fmm2d.cu",
+           "operators.cu",
            "dist.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

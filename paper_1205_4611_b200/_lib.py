@@ -68,6 +68,22 @@ _SIGS = {
     "fmm2d_export_expansions": (C.c_int, [C.c_void_p, _dp, _dp]),
     "fmm2d_export_phi": (C.c_int, [C.c_void_p, _dp]),
     "fmm2d_direct": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]),
+    # unit operators and per-level connectivity (operators.py, connectivity.py:47-96)
+    "fmm2d_op_p2m": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _dp, _dp, _dp, C.c_int, _dp]),
+    "fmm2d_op_p2l": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _dp, _dp, _dp, C.c_int, _dp]),
+    "fmm2d_op_m2m": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, _dp, _dp, C.c_int]),
+    "fmm2d_op_l2l": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, _dp, _dp]),
+    "fmm2d_op_m2l": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, _dp, _dp, _dp]),
+    "fmm2d_op_l2p": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp, C.c_int64, _dp, _dp]),
+    "fmm2d_op_m2p": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp, C.c_int64, _dp, _dp]),
+    "fmm2d_op_reciprocal_parts": (C.c_int, [C.c_void_p, C.c_int64, _dp, C.c_int64, _dp, _dp,
+                                            _dp, _i64p]),
+    "fmm2d_op_kernel_block": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp,
+                                        _i64p]),
+    "fmm2d_classify_level": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, _dp, _i64p, _i64p,
+                                       C.c_double, _i64p, _i64p, _i64p, _i64p]),
+    "fmm2d_reclassify_finest": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, _dp, _i64p, _i64p,
+                                          C.c_double] + [_i64p] * 6),
     # distributed evaluation (one rank; collectives issued by the caller)
     "fmm2d_dist_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_double,
                                    C.c_int, C.c_void_p, C.POINTER(C.c_int32)]),

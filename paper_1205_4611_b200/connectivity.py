@@ -29,7 +29,11 @@ class InteractionLists:
 
 
 def _split(off: np.ndarray, idx: np.ndarray) -> list[np.ndarray]:
-    return np.split(idx, off[1:-1] - off[0]) if off.size > 1 else []
+    if off.size <= 1:
+        return []
+    if off.size == 2:
+        return [idx]
+    return np.split(idx, off[1:-1] - off[0])
 
 
 def export_lists(ctx: _lib.Context, n_levels: int) -> InteractionLists:
@@ -55,6 +59,64 @@ def export_lists(ctx: _lib.Context, n_levels: int) -> InteractionLists:
     p2l = _split(arrs[2], arrs[3])
     m2p = _split(arrs[4], arrs[5])
     return InteractionLists(n_levels, weak, p2p, p2l, m2p)
+
+
+def _csr_of(lists) -> tuple[np.ndarray, np.ndarray]:
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([np.size(a) for a in lists])
+    idx = (np.concatenate([np.asarray(a, np.int64) for a in lists]) if len(lists)
+           else np.zeros(0, np.int64))
+    return off, np.ascontiguousarray(idx, np.int64)
+
+
+def _level_geometry(lv):
+    return (np.ascontiguousarray(lv.center, np.complex128),
+            np.ascontiguousarray(lv.half_width, np.float64),
+            np.ascontiguousarray(lv.half_height, np.float64))
+
+
+def classify_level(tree: FmmTree, level: int, parent_strong: list[np.ndarray], theta: float,
+                   *, device: int | None = None):
+    """Split each box's inherited candidates into (strong, weak) lists
+    (connectivity.py:47-68): candidates of box b are the children of the
+    boxes in ``parent_strong[b // 4]``, ascending; the θ-criterion
+    (bit-exact glibc hypot / numpy cabs restatement) runs on the GPU."""
+    lv = tree.levels[level]
+    c, hw, hh = _level_geometry(lv)
+    poff, pidx = _csr_of(parent_strong)
+    ncand = 16 * int(poff[-1])          # 4 children per parent, 4 candidates per entry
+    woff = np.empty(lv.n_boxes + 1, np.int64)
+    soff = np.empty(lv.n_boxes + 1, np.int64)
+    widx = np.empty(ncand, np.int64)
+    sidx = np.empty(ncand, np.int64)
+    ctx = _lib.default_context(device)
+    with ctx.lock:
+        ctx.check(ctx.lib.fmm2d_classify_level(
+            ctx.h, lv.n_boxes, _lib.dptr(c.view(np.float64)), _lib.dptr(hw), _lib.dptr(hh),
+            _lib.iptr(poff), _lib.iptr(pidx), float(theta), _lib.iptr(woff), _lib.iptr(widx),
+            _lib.iptr(soff), _lib.iptr(sidx)))
+    strong = _split(soff, sidx[:soff[-1]])
+    weak = _split(woff, widx[:woff[-1]])
+    return strong, weak
+
+
+def reclassify_finest(tree: FmmTree, strong: list[np.ndarray], theta: float, *,
+                      device: int | None = None):
+    """Refine finest strong pairs into (p2p, p2l, m2p) (connectivity.py:71-96):
+    a non-self pair passing the swapped test with unequal radii moves to p2l
+    (larger source) or m2p (smaller source); on the GPU."""
+    lv = tree.levels[tree.n_levels]
+    c, hw, hh = _level_geometry(lv)
+    soff, sidx = _csr_of(strong)
+    n = int(soff[-1])
+    outs = [np.empty(lv.n_boxes + 1, np.int64) if k % 2 == 0 else np.empty(n, np.int64)
+            for k in range(6)]
+    ctx = _lib.default_context(device)
+    with ctx.lock:
+        ctx.check(ctx.lib.fmm2d_reclassify_finest(
+            ctx.h, lv.n_boxes, _lib.dptr(c.view(np.float64)), _lib.dptr(hw), _lib.dptr(hh),
+            _lib.iptr(soff), _lib.iptr(sidx), float(theta), *[_lib.iptr(a) for a in outs]))
+    return tuple(_split(outs[k], outs[k + 1][:outs[k][-1]]) for k in (0, 2, 4))
 
 
 def build_connectivity(tree: FmmTree, theta: float, *, device: int | None = None

@@ -27,6 +27,9 @@ constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
 #ifndef P2P_HI
 #define P2P_HI 1
 #endif
+#ifndef P2P_EXACT
+#define P2P_EXACT 0
+#endif
 
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -58,6 +61,27 @@ __device__ __forceinline__ double rcp_nr(double x) {
 __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double yx, double yy,
                                          double& bx, double& by, int& skips) {
   const double dx = zx - yx, dy = zy - yy;
+#if P2P_EXACT
+  // the reference's rounding sequence (operators.py:265-272, 291): r2 = dx*dx;
+  // r2 += dy*dy (two rounded products, one rounded add); s = 1/r2; the dot
+  // product accumulates (dx*s)*g; only r2 == 0 is skipped
+  const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  const bool zero = r2 == 0.0;
+  skips += zero;
+#if P2P_EXACT > 1
+  const double s = __drcp_rn(zero ? 1.0 : r2);
+#else
+  // MUFU seed (1/1 for a zero high word) + one cubic Newton step
+  int hi = __double2hiint(r2);
+  hi = hi == 0 ? 1072693248 : hi;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(__hiloint2double(hi, 0)));
+  const double e = fma(-r2, y, 1.0);
+  const double s = fma(fma(e, e, e), y, y);
+#endif
+  bx = fma(__dmul_rn(dx, s), g, bx);
+  by = fma(__dmul_rn(dy, s), g, by);
+#else
   double r2 = fma(dx, dx, dy * dy);
 #if P2P_HI
   // r2 >= 0, so its high word is zero only for 0 or a denormal (which
@@ -81,6 +105,7 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
 #endif
   bx = fma(gs, dx, bx);
   by = fma(gs, dy, by);
+#endif
 }
 
 // sum of the staged sources [j0, j1) on target y into (ax, ay): 4-way

@@ -188,6 +188,14 @@ def direct_evaluate(points: ParticleSet, symmetric: bool = False, *,
     return out
 
 
+def _p2m_all(tree, p: int) -> np.ndarray:
+    """Batched P2M of every finest box (engine.py:67-82) on the GPU:
+    complex128[4**L, p+1] about the box centers."""
+    from .operators import p2m_boxes
+    lv = tree.finest
+    return p2m_boxes(tree.src_pos, tree.src_strength, lv.src_offsets, lv.center, p)
+
+
 def max_rel_error(approx, exact) -> float:
     """max |a - e| / |e| over nonzero e (engine.py:326-341)."""
     approx = np.asarray(approx)
