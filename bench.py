@@ -296,7 +296,7 @@ def run_ours(args, cfg, ws, rank, local):
         # compute roof: on B200 the FP64 tensor (DMMA) peak equals the DFMA vector
         # peak (one shared FP64 pipe, profiles/r01_fp64_peak.json); the kernel
         # runs on the vector pipe
-        "roofline": {"kernel": "m2l", "bound": "tensor", "pipe": "fp64 (DMMA = DFMA peak)",
+        "roofline": {"kernel": "m2l", "bound": "fp64", "pipe": "fp64 (DMMA = DFMA peak)",
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("k_m2l_dense", args.config),
@@ -417,7 +417,7 @@ def run_dist(args, cfg, ws, rank, local):
         "e2e": {"value": n_total / e2e_s, "unit": "particles/s",
                 "h2d_bytes_per_step": 24 * (hi - lo), "d2h_bytes_per_step": 24 * len(own),
                 "ms_per_step": e2e_s * 1e3},
-        "roofline": {"kernel": "m2l", "bound": "tensor", "pipe": "fp64 (DMMA = DFMA peak)",
+        "roofline": {"kernel": "m2l", "bound": "fp64", "pipe": "fp64 (DMMA = DFMA peak)",
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                      "algorithmic": f"rank-0 M2L pairs {pairs} x {m2l_flops_per_pair(cfg['p'])} "
@@ -430,38 +430,87 @@ def run_dist(args, cfg, ws, rank, local):
     return out if rank == 0 else None
 
 
+REF_SITE = ROOT / "oracle" / "_ref" / "site"    # oracle/build_ref.sh (test/bench infrastructure)
+
+
+def _import_reference():
+    """The reference package itself (staged by oracle/build_ref.sh; travels to
+    the GPU box with the snapshot).  None when it was not staged."""
+    if not (REF_SITE / "fmm2d").is_dir():
+        return None
+    if str(REF_SITE) not in sys.path:
+        sys.path.insert(0, str(REF_SITE))
+    import fmm2d
+    return fmm2d
+
+
+def _reference_points(fmm2d, cfg, n):
+    """The bench inputs from the reference's own generator (datasets.py:53-78):
+    sources seed 0, separate evaluation points seed 1 (C4)."""
+    from fmm2d.datasets import DistributionSpec, sample_points
+    from fmm2d.tree import ParticleSet
+    pts = sample_points(DistributionSpec(cfg["kind"], 0.01, 0), n)
+    if cfg["m"] is not None:
+        ev = sample_points(DistributionSpec(cfg["kind"], 0.01, 1), n).positions
+        pts = ParticleSet(pts.positions, pts.strengths, ev)
+    return pts
+
+
+def _ref_single_core(job):
+    """Subprocess body: the reference's fmm_evaluate, sequential
+    (parallel=False), pinned to one host core with single-threaded BLAS."""
+    cfg, n = job
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    fmm2d = _import_reference()
+    from fmm2d.tree import TreeConfig
+    pts = _reference_points(fmm2d, cfg, n)
+    t0 = time.perf_counter()
+    _, rep = fmm2d.fmm_evaluate(pts, TreeConfig(35, 0.5, cfg["p"]), parallel=False)
+    return time.perf_counter() - t0, {k: round(v, 3) for k, v in rep.phase_seconds.items()}
+
+
+CPU_FULL_MAX_N = 1_000_000    # the 1-core leg runs the full config up to C2-C4 size (~45-75 s)
+
+
 def cpu_baseline(cfg, n_sample):
-    """Oracle port of the reference CPU path on a bounded sample of the same
-    workload (same distribution and p, N = n_sample)."""
+    """The reference's CPU path on one host core: its own
+    fmm_evaluate, parallel=False, OPENBLAS_NUM_THREADS=1, same inputs and
+    config as the GPU line when N <= 1e6 (C5: a 1e6-point sample).  Falls back
+    to the oracle port when the reference was not staged."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    n = cfg["n"] if cfg["n"] <= CPU_FULL_MAX_N else min(n_sample, CPU_FULL_MAX_N)
+    if _import_reference() is not None:
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        with cf.ProcessPoolExecutor(1, mp_context=mp.get_context("spawn")) as pool:
+            dt, phases = pool.submit(_ref_single_core, (cfg, n)).result()
+        same = n == cfg["n"]
+        return {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "reference",
+                "same_config": same,
+                "sample": f"reference fmm2d.fmm_evaluate (oracle/_ref/site), parallel=False, "
+                          f"1 core, OPENBLAS_NUM_THREADS=1, {cfg['kind']} N={n}"
+                          f"{'' if cfg['m'] is None else ' M=N separate'}, p={cfg['p']}: "
+                          f"one call, {dt:.1f} s"
+                          + ("" if same else f" (bounded sample of N={cfg['n']})"),
+                "phase_seconds": phases}
     from oracle import fmm2d_oracle as O
     import paper_1205_4611_b200 as F
     n = min(n_sample, cfg["n"])
     pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 0), n)
     ev = None
     if cfg["m"] is not None:
-        ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 1), min(n_sample, cfg["m"])).positions
+        ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 1), n).positions
     t0 = time.perf_counter()
     O.fmm(pts.positions, pts.strengths, ev, 35, 0.5, cfg["p"])
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": "particles/s", "cores": 1, "kind": "port",
-            "sample": f"oracle/fmm2d_oracle.py full pipeline on {cfg['kind']} N={n} "
-                      f"(M={'N' if ev is None else len(ev)}), p={cfg['p']}, one call, {dt:.2f} s, "
-                      "numpy single-threaded"}
-
-
-def _ref_worker(job):
-    """One host core: the oracle port of the reference path on its own sample."""
-    kind, n, m, p, seed, reps = job
-    import paper_1205_4611_b200.datasets as D
-    from oracle import fmm2d_oracle as O
-    pts = D.sample_points(D.DistributionSpec(kind, 0.01, seed), n)
-    ev = None if m is None else D.sample_points(D.DistributionSpec(kind, 0.01, seed + 7919), m).positions
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.fmm(pts.positions, pts.strengths, ev, 35, 0.5, p)
-        ts.append(time.perf_counter() - t0)
-    return ts
+            "same_config": False,
+            "sample": f"oracle port (reference not staged) on {cfg['kind']} N={n}, p={cfg['p']}, "
+                      f"one call, {dt:.2f} s, numpy single-threaded"}
 
 
 def host_cores():
@@ -472,40 +521,51 @@ def host_cores():
 
 
 def run_reference(args, cfg, ws, rank):
-    """The reference's CPU path (oracle port: /root/reference does not exist on
-    the GPU box) with every host core: one independent bounded sample per core
-    (OpenBLAS pinned to one thread per process), throughput = all particles of
-    a step / the slowest core's time.  Independent problems are the most
-    favourable use of the cores for the reference, whose own thread pool
-    (engine.py:50-64) scales poorly (8 workers, 43.5 -> 33.3 s)."""
+    """The reference arm: the UNMODIFIED reference package (oracle/_ref/site,
+    staged from /root/reference/pkg by oracle/build_ref.sh) through its public
+    API fmm2d.fmm_evaluate on the bench's own config and inputs, with every
+    host core: parallel=True, n_workers = cores (the
+    reference's thread pool, engine.py:50-64, 214-215).  Each timed step is one
+    full evaluation (the same N as the GPU line).  Warm-up steps (imports,
+    allocator) evaluate a 1e4-point problem of the same distribution.  Under
+    torchrun only rank 0 runs."""
     if rank != 0:
         return None
-    import concurrent.futures as cf
-    import multiprocessing as mp
-    n = min(args.cpu_n, cfg["n"])
-    m = None if cfg["m"] is None else n
+    fmm2d = _import_reference()
+    if fmm2d is None:
+        return {"impl": "reference",
+                "unavailable": "oracle/_ref/site not staged (run oracle/build_ref.sh)"}
+    from fmm2d.tree import TreeConfig
     cores = max(1, min(host_cores(), args.ref_cores or host_cores()))
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
-    reps = args.warmup + args.steps
-    with cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as pool:
-        res = list(pool.map(_ref_worker, [(cfg["kind"], n, m, cfg["p"], 1000 + q, reps)
-                                          for q in range(cores)]))
-    # per step: the slowest core bounds the step
-    step_s = [max(r[args.warmup + k] for r in res) for k in range(args.steps)]
-    ms = 1e3 * sum(step_s) / len(step_s)
-    val = cores * n / (ms * 1e-3)
-    sample = (f"oracle port of the reference CPU path on {cores} host cores, one {cfg['kind']} "
-              f"N={n} p={cfg['p']} problem per core per step (bounded sample of {args.config}), "
-              "numpy + OpenBLAS single-threaded per process")
+    n = cfg["n"]
+    tcfg = TreeConfig(35, 0.5, cfg["p"])
+    warm = _reference_points(fmm2d, cfg, min(n, 10_000))
+    for _ in range(args.warmup):
+        fmm2d.fmm_evaluate(warm, tcfg, parallel=True, n_workers=cores)
+    pts = _reference_points(fmm2d, cfg, n)
+    secs, phases = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, rep = fmm2d.fmm_evaluate(pts, tcfg, parallel=True, n_workers=cores)
+        secs.append(time.perf_counter() - t0)
+        phases.append(rep.phase_seconds)
+    ms = 1e3 * sum(secs) / len(secs)
+    val = n / (ms * 1e-3)
+    phase_mean = {k: round(sum(ph[k] for ph in phases) / len(phases), 3) for k in phases[0]}
+    sample = (f"reference fmm2d.fmm_evaluate (oracle/_ref/site), parallel=True, "
+              f"n_workers={cores}, full {args.config} problem ({cfg['kind']} N={n}"
+              f"{'' if cfg['m'] is None else ' M=N separate'}, p={cfg['p']}) per step")
     return {"metric": METRIC, "value": val, "unit": "particles/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
+            "data": "synthetic (reference sample_points, seed 0)", "impl": "reference",
             "config": {"workload": cfg["desc"], "name": args.config, "n_sources": n,
-                       "p": cfg["p"], "cores": cores},
-            "cpu_baseline": {"value": val, "unit": "particles/s", "cores": cores, "kind": "port",
-                             "sample": sample},
+                       "n_evals": n if cfg["m"] is not None else n, "p": cfg["p"], "theta": 0.5,
+                       "n_desired": 35, "distribution": cfg["kind"], "cores": cores,
+                       "warmup_sample": "N=1e4 of the same distribution"},
+            "phase_seconds": phase_mean,
+            "cpu_baseline": {"value": val, "unit": "particles/s", "cores": cores,
+                             "kind": "reference", "same_config": True, "sample": sample},
             "e2e": {"value": val, "unit": "particles/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -518,7 +578,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--npoints", type=int, default=None, help="override N (and M)")
-    ap.add_argument("--cpu-n", type=int, default=100_000, help="CPU baseline sample size")
+    ap.add_argument("--cpu-n", type=int, default=1_000_000,
+                    help="CPU baseline sample size when the config exceeds 1e6 points")
     ap.add_argument("--ref-cores", type=int, default=0,
                     help="host cores for --impl reference (default: all available)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

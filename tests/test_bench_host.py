@@ -14,12 +14,16 @@ import bench  # noqa: E402
 
 def test_reference_arm_json():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "1", "--cpu-n", "3000", "--ref-cores", "2"],
+                          "--steps", "1", "--warmup", "1", "--npoints", "3000", "--ref-cores", "2"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert res.returncode == 0, res.stderr[-2000:]
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "particles/s"
     assert line["value"] > 0 and line["cpu_baseline"]["cores"] == 2
+    # the reference itself (oracle/_ref/site) on the bench's own config and N
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["cpu_baseline"]["same_config"] is True
+    assert line["config"]["n_sources"] == 3000 and line["config"]["p"] == 20
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["metric"] == bench.METRIC
 
