@@ -35,6 +35,24 @@ bool m2l_force_target() {
   }();
   return v;
 }
+// FMM2D_M2L=dmma selects the FP64 tensor-core kernel (measured slower than the
+// DFMA dense kernel on B200: profiles/r02/m2l_dmma_vs_dense.txt)
+bool m2l_dmma() {
+  static bool v = [] {
+    const char* e = getenv("FMM2D_M2L");
+    return e && std::string(e) == "dmma";
+  }();
+  return v;
+}
+// cudaFuncSetAttribute is per device: remember which devices have it
+template <class K>
+void ensure_smem_attr(K kernel, int bytes, unsigned& done_mask) {
+  int dev = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  if (dev < 32 && (done_mask >> dev) & 1u) return;
+  FMM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  if (dev < 32) done_mask |= 1u << dev;
+}
 
 int sm_count() {
   static int sms = [] {
@@ -500,6 +518,165 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   }
 }
 
+// M2L on the FP64 tensor cores (mma.sync m16n8k4 .f64, DMMA).  The dense
+// Pascal-matrix form above is a real GEMM per item: rows = (re, im) of the
+// prescaled alpha_k of 8 pairs (A, 16 x 4 per k-step), columns = output
+// coefficients j (B = T[j][k-1] = C(j+k-1, k-1), a constant matrix held in
+// registers as KT x NT fragments for the whole kernel), so the ~2p(p+1) FMAs
+// per pair issue as KT*NT/8 DMMA instructions per pair instead of ~840 DFMA
+// (p=20: 15 DMMA per 8 pairs).  Prescale (alpha_k = a_k q^k, q = -1/rho) and
+// postscale (b_j = c_j / rho^j) stay on the DFMA pipe; each thread of a quad
+// (lane & 3) handles the k's / j's its fragments own.  The per-target fold
+// (SMEM rows, ordered segment sums, partials + k_m2l_fixup for targets
+// spanning items) is the dense kernel's, unchanged.  Fragment layouts
+// (PTX ISA, mma.m16n8k4 .f64): a0 = A[g][tig], a1 = A[g+8][tig];
+// b0 = B[tig][g]; c{0,1} = C[g][2 tig + {0,1}], c{2,3} = C[g+8][2 tig + {0,1}]
+// with g = lane >> 2, tig = lane & 3.
+template <int PM>
+struct M2LDmmaCfg {
+  static constexpr int KT = (PM + 3) / 4;          // k-steps over k = 1..PM
+  static constexpr int NT = (PM + 1 + 7) / 8;      // n-tiles over j = 0..PM
+  static constexpr int R = 2 * (PM + 1);
+  static constexpr int STR = M2L_ITEM + 1;
+  static constexpr int SMEM = R * STR * 8;
+  static constexpr int MT = M2L_ITEM / 2 / 8;      // m-tiles (8 pairs) per warp per item
+  static constexpr int MINB = PM <= 24 ? 8 : 5;    // B fragments: KT*NT registers pairs
+};
+
+__device__ __forceinline__ void dmma_m16n8k4(double (&d)[4], double a0, double a1, double b) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+template <int PM>
+__global__ void __launch_bounds__(M2L_ITEM, M2LDmmaCfg<PM>::MINB)
+k_m2l_dmma(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
+           const int* __restrict__ w_tgt, const double* __restrict__ cx,
+           const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
+           double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+  pdl_enter();
+  static_assert(M2L_ITEM == 64, "two warps x 4 m-tiles of 8 pairs");
+  using Cfg = M2LDmmaCfg<PM>;
+  if (lists_overflowed(st)) return;
+  extern __shared__ double red[];                 // [R][STR]
+  __shared__ int s_t[M2L_ITEM];
+  __shared__ int s_seg[M2L_ITEM + 1];
+  __shared__ int s_nseg;
+  __shared__ int s_wcnt[M2L_ITEM / 32];
+  const long long npairs = *total_ptr;
+  const long long nitems = (npairs + M2L_ITEM - 1) / M2L_ITEM;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  double bf[Cfg::KT][Cfg::NT];                     // B = T[j][k-1], j = 8 nt + g, k = 4 ks + tig + 1
+#pragma unroll
+  for (int ks = 0; ks < Cfg::KT; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      const int j = nt * 8 + g, k = ks * 4 + tig + 1;
+      bf[ks][nt] = (j <= PM && k <= PM) ? c_m2l_tab<PM>.v[j][k - 1] : 0.0;
+    }
+  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const long long i_own = item * M2L_ITEM + tid;
+    const int t_own = i_own < npairs ? __ldg(w_tgt + i_own) : -1;
+    const int prev_t = item > 0 ? __ldg(w_tgt + item * M2L_ITEM - 1) : -1;
+    const long long nxt = (item + 1) * M2L_ITEM;
+    const int next_t = nxt < npairs ? __ldg(w_tgt + nxt) : -1;
+#pragma unroll 1
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      const int slot = wid * 32 + mt * 8 + g;
+      const long long i = item * M2L_ITEM + slot;
+      const bool valid = i < npairs;
+      const int t = valid ? __ldg(w_tgt + i) : 0;
+      const int s = valid ? __ldg(w_src + i) : 0;
+      const double rx = cx[s] - cx[t], ry = cy[s] - cy[t];        // source - target
+      const bool sing = valid && rx == 0.0 && ry == 0.0;
+      if (sing && tig == 0) atomicOr(&st->flags, ST_M2L_SINGULAR);
+      const cplx inv = (valid && !sing) ? crcp_fast(cplx{rx, ry}) : cplx{0.0, 0.0};
+      const cplx q{-inv.x, -inv.y};
+      const cplx q2 = cmul(q, q), q3 = cmul(q2, q), q4 = cmul(q2, q2);
+      cplx qk = tig == 0 ? q : (tig == 1 ? q2 : (tig == 2 ? q3 : q4));   // q^(tig+1)
+      const double2* a = mult + (long long)s * (p + 1);
+      double acc[Cfg::NT][4];
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < Cfg::KT; ++ks) {
+        const int k = ks * 4 + tig + 1;
+        const double2 ak = k <= p ? a[k] : make_double2(0.0, 0.0);
+        const cplx al = cmul(cplx{ak.x, ak.y}, qk);                  // alpha_k (operators.py:203-206)
+        qk = cmul(qk, q4);
+#pragma unroll
+        for (int nt = 0; nt < Cfg::NT; ++nt) dmma_m16n8k4(acc[nt], al.x, al.y, bf[ks][nt]);
+      }
+      // b_j = c_j inv^j for j = 8 nt + 2 tig + e (operators.py:218-219)
+      const cplx i2 = cmul(inv, inv), i4 = cmul(i2, i2), i8 = cmul(i4, i4);
+      cplx w = tig == 0 ? cplx{1.0, 0.0} : (tig == 1 ? i2 : (tig == 2 ? i4 : cmul(i4, i2)));
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) {
+        const cplx w1 = cmul(w, inv);
+        const int j0 = nt * 8 + 2 * tig;
+        const cplx b0 = cmul(cplx{acc[nt][0], acc[nt][2]}, w);
+        const cplx b1 = cmul(cplx{acc[nt][1], acc[nt][3]}, w1);
+        if (j0 <= PM) {
+          red[(2 * j0) * Cfg::STR + slot] = b0.x;
+          red[(2 * j0 + 1) * Cfg::STR + slot] = b0.y;
+        }
+        if (j0 + 1 <= PM) {
+          red[(2 * j0 + 2) * Cfg::STR + slot] = b1.x;
+          red[(2 * j0 + 3) * Cfg::STR + slot] = b1.y;
+        }
+        w = cmul(w, i8);
+      }
+    }
+    s_t[tid] = t_own;
+    __syncthreads();
+    const bool valid = t_own >= 0;
+    const int t = t_own;
+    const bool start = valid && (tid == 0 || s_t[tid - 1] != t);
+    const unsigned bal = __ballot_sync(0xffffffffu, start);
+    if (lane == 0) s_wcnt[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < M2L_ITEM / 32; ++w2) before += w2 < wid ? s_wcnt[w2] : 0;
+    if (start) s_seg[before + __popc(bal & ((1u << lane) - 1))] = tid;
+    if (tid == M2L_ITEM - 1) {
+      int tot = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < M2L_ITEM / 32; ++w2) tot += s_wcnt[w2];
+      s_nseg = tot;
+      s_seg[tot] = (int)min((long long)M2L_ITEM, npairs - item * M2L_ITEM);
+    }
+    __syncthreads();
+    const int nseg = s_nseg;
+    const int R = 2 * (p + 1);
+    const bool first_cont = item > 0 && prev_t == s_t[0];
+    const int nvalid = s_seg[nseg];
+    const bool last_cont = nvalid == M2L_ITEM && next_t >= 0 && next_t == s_t[nvalid - 1];
+    for (int task = tid; task < nseg * R; task += M2L_ITEM) {
+      const int sg = task / R, r = task - sg * R;
+      const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
+      const double* row = red + r * Cfg::STR;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int qq = q0;
+      for (; qq + 4 <= q1; qq += 4) {
+        a0 += row[qq];
+        a1 += row[qq + 1];
+        a2 += row[qq + 2];
+        a3 += row[qq + 3];
+      }
+      if (qq < q1) a0 += row[qq];
+      if (qq + 1 < q1) a1 += row[qq + 1];
+      if (qq + 2 < q1) a2 += row[qq + 2];
+      m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1,
+               (a0 + a1) + (a2 + a3), sg == 0 && first_cont, sg == nseg - 1 && last_cont);
+    }
+    __syncthreads();
+  }
+}
+
 // Target-owned M2L (default).  One warp per target box walks the target's
 // weak list in chunks of 16 pairs; lane pair (2i, 2i+1) carries the real /
 // imaginary part of pair i (the cascades of operators.py:339-344 are
@@ -807,19 +984,28 @@ struct Launch {
       E.partials.reserve(sizeof(double2) * 2 * items * (E.p + 1));
       E.item_flags.reserve(((items + 4) & ~3ll) + 8);
       FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
-      static bool attr = false;
-      if (!attr) {
-        FMM_CUDA(cudaFuncSetAttribute(k_m2l_dense<PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Cfg::SMEM));
-        attr = true;
+      if (m2l_dmma()) {
+        using DC = M2LDmmaCfg<PM>;
+        static unsigned attr_dmma = 0;
+        ensure_smem_attr(k_m2l_dmma<PM>, DC::SMEM, attr_dmma);
+        const unsigned grid = (unsigned)std::min<long long>(
+            std::max(1ll, items), (long long)M2L_GRID_WAVES * DC::MINB * sm_count());
+        note_launch();
+        launch(k_m2l_dmma<PM>, grid, M2L_ITEM, DC::SMEM, st,
+            total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
+            T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
+            E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
+      } else {
+        static unsigned attr_dense = 0;
+        ensure_smem_attr(k_m2l_dense<PM>, Cfg::SMEM, attr_dense);
+        const unsigned grid = (unsigned)std::min<long long>(
+            std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
+        note_launch();
+        launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st,
+            total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
+            T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
+            E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
       }
-      const unsigned grid = (unsigned)std::min<long long>(
-          std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
-      note_launch();
-      launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st, 
-          total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
-          T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
-          E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
       note_launch();
       launch(k_m2l_fixup, std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st, 
           total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
