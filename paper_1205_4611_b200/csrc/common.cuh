@@ -37,6 +37,7 @@ struct DevStatus {
   int max_len[4];                         // weak, p2p, p2l, m2p list lengths
   int overflow_where;
   int pad1;
+  int list_total[4];                      // CSR totals (weak, p2p, p2l, m2p), end of call
 };
 
 // list buffers overflowed earlier in this stream: every list consumer bails out

@@ -675,8 +675,9 @@ __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
   else if (i > hi) off[i] = off[hi];
 }
 
-__global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx) {
+__global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx, unsigned* lb_base) {
   pdl_enter();
+  lb_advance_base(lb_base);   // this evaluation's look-back epoch base (lookback.cuh)
   weak_off[0] = 0;
   weak_off[1] = 0;     // the root has no far field (connectivity.py:106)
   s_off[0] = 0;
@@ -765,12 +766,13 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     FMM_CUDA(cudaMemsetAsync(Ls.lb_ticket.p, 0, sizeof(unsigned) * 4, st));
     Ls.lb_tiles = max_tiles;
   }
+  unsigned* lb_base = lb_base_prepare(Ls.lb_base, Ls.lb_base_ready, st);
+  Ls.lb_epoch = 0;
   auto lbstate = [&]() {
-    Ls.lb_epoch = (Ls.lb_epoch + 1) & 0x3fffffffu;
-    if (Ls.lb_epoch == 0) Ls.lb_epoch = 1;
+    ++Ls.lb_epoch;
     long long* v = Ls.lb_vals.as<long long>();
     return LookbackState{Ls.lb_flags.as<unsigned>(), v, v + 3 * max_tiles,
-                         Ls.lb_ticket.as<unsigned>(), Ls.lb_epoch};
+                         Ls.lb_ticket.as<unsigned>(), Ls.lb_epoch, lb_base};
   };
 
   const LevelGeo geo{T.box_cx.as<double>(), T.box_cy.as<double>(), T.box_r.as<double>()};
@@ -783,7 +785,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     Ls.cl_mask.reserve(sizeof(unsigned) * std::max(4 * mplane, 2 * rplane));
   }
   note_launch();
-  launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>());
+  launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>(), lb_base);
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
     const long long tb = part.lo(l), te = part.hi(l);
@@ -864,6 +866,17 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   }
 }
 
+__global__ void k_list_totals(const int* w, const int* a, const int* b, const int* c,
+                              DevStatus* st) {
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    st->list_total[0] = *w;
+    st->list_total[1] = *a;
+    st->list_total[2] = *b;
+    st->list_total[3] = *c;
+  }
+}
+
 void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st,
                const Part& part) {
   const int L = T.L;
@@ -889,7 +902,10 @@ void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t
   hist(Ls.p2p_off.as<int>() + f0, f1 - f0, 1);
   hist(Ls.p2l_off.as<int>() + f0, f1 - f0, 2);
   hist(Ls.m2p_off.as<int>() + f0, f1 - f0, 3);
-  (void)nleaf;
+  // the totals travel with the status word (no extra host round trips)
+  note_launch();
+  launch(k_list_totals, 1, 32, 0, st, Ls.weak_off.as<int>() + nbox, Ls.p2p_off.as<int>() + nleaf,
+         Ls.p2l_off.as<int>() + nleaf, Ls.m2p_off.as<int>() + nleaf, dstat);
 }
 
 }  // namespace fmm

@@ -45,6 +45,23 @@ struct DistState {
 
 using namespace fmm;
 
+// one instantiated CUDA graph of the evaluation pipeline (fmm2d.cu), valid for
+// the exact configuration and device buffers it was captured with
+struct GraphCache {
+  bool valid = false;
+  std::vector<long long> key;
+  std::vector<cudaGraphExec_t> seg;  // segments, launched in order on ctx->st
+  std::vector<int> act;              // host action after each segment (ACT_*)
+  long long launches = 0;            // kernels inside (captured count)
+  std::vector<std::vector<long long>> failed;   // keys whose capture failed: stay eager
+  void clear() {
+    for (auto e : seg) cudaGraphExecDestroy(e);
+    seg.clear();
+    act.clear();
+    valid = false;
+  }
+};
+
 struct fmm2d_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -58,6 +75,10 @@ struct fmm2d_ctx {
   ExpState E;
   DBuf d_status;
   DevStatus* h_status = nullptr;
+  DevStatus* h_status_init = nullptr;  // constant reset image (graph-replay safe)
+  GraphCache graph;
+  cudaEvent_t ev_d2h = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;   // upward-pass side stream dependencies
   int* h_hist = nullptr;
   cudaEvent_t ev[10] = {};
   cudaEvent_t ev_side[3] = {};      // P2M / M2M on the tree's side stream (overlapped)
@@ -92,11 +113,7 @@ int guarded(fmm2d_ctx* c, F&& f) {
 }
 
 inline void reset_status(fmm2d_ctx* c) {
-  DevStatus init;
-  std::memset(&init, 0, sizeof init);
-  init.degenerate_key = ~0ull;
-  *c->h_status = init;
-  FMM_CUDA(cudaMemcpyAsync(c->d_status.p, c->h_status, sizeof(DevStatus),
+  FMM_CUDA(cudaMemcpyAsync(c->d_status.p, c->h_status_init, sizeof(DevStatus),
                            cudaMemcpyHostToDevice, c->st));
 }
 

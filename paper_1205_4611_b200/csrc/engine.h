@@ -127,7 +127,9 @@ struct TreeState {
   DBuf tile_cnt, tile_pre;
   DBuf lb_flags, lb_vals, lb_ticket;  // look-back state of the fused partition steps
   long long lb_tiles = 0;
-  unsigned lb_epoch = 0;
+  unsigned lb_epoch = 0;             // launch index within the evaluation
+  DBuf lb_base;                      // device epoch base (lookback.cuh)
+  bool lb_base_ready = false;
   DBuf rect_tab, cut_tab, axis_tab;
   DBuf leaf_of;                      // eval/source leaf ids (fallback + evals)
   // outputs (tree order)
@@ -155,7 +157,9 @@ struct ListState {
   DBuf lb_flags, lb_vals, lb_ticket;  // single-pass look-back state of the list kernels
   DBuf cl_cnt, cl_mask;              // split classify: per-target counts, far masks
   long long lb_tiles = 0;
-  unsigned lb_epoch = 0;
+  unsigned lb_epoch = 0;             // launch index within the evaluation
+  DBuf lb_base;                      // device epoch base (lookback.cuh)
+  bool lb_base_ready = false;
   DBuf p2p_off, p2p_idx, p2l_off, p2l_idx, m2p_off, m2p_idx;  // finest, level-local ids
   DBuf totals;                       // int64 scratch for scans
   DBuf hist;                         // int32 histograms [4][HIST_BINS]
@@ -175,6 +179,18 @@ struct ExpState {
 
 // count of engine kernel launches (gpu_launches evidence in the report)
 extern long long g_launches;
+extern unsigned long long g_dbuf_gen;   // bumped on every device (re)allocation
+// CUDA-graph capture of the evaluation (fmm2d.cu): a phase that needs a host
+// action between two kernels calls capture_cut(); while capturing it closes
+// the current graph segment (the replay performs the action between segment
+// launches) and returns true; otherwise it returns false and the caller
+// performs the action itself.
+enum : int { ACT_NONE = 0, ACT_WAIT_INPUTS = 1, ACT_D2H = 2 };
+bool capture_cut(int action);
+// device epoch base of a look-back state: allocated + zeroed once, then
+// advanced by one kernel per evaluation (graph-replay safe epoch tags)
+unsigned* lb_base_prepare(DBuf& buf, bool& ready, cudaStream_t st);
+void lb_advance(unsigned* base, cudaStream_t st);
 inline void note_launch() { ++g_launches; }
 
 // launch an engine kernel with programmatic dependent launch (see pdl_enter)

@@ -16,8 +16,23 @@ struct LookbackState {
   long long* aggv;       // [ntiles * NW]
   long long* incv;       // [ntiles * NW]
   unsigned* ticket;      // one counter, 0 between launches
-  unsigned epoch;        // nonzero, distinct per launch
+  unsigned epoch;        // launch index within the evaluation (1 .. LB_EPOCH_STRIDE-1)
+  const unsigned* base;  // device word advanced by LB_EPOCH_STRIDE per evaluation
 };
+
+// Epoch tags: a per-evaluation device-side base plus the launch's index
+// within the evaluation.  Kernel arguments therefore repeat exactly from one
+// evaluation to the next (a captured CUDA graph replays them unchanged) while
+// the tags stay distinct across evaluations (flags are never cleared).
+constexpr unsigned LB_EPOCH_STRIDE = 4096;
+__device__ __forceinline__ unsigned lb_tag_epoch(unsigned local, const unsigned* base) {
+  const unsigned e = (local + (base ? __ldcg(base) : 0u)) & 0x3fffffffu;
+  return e ? e : 1u;
+}
+// one thread: advance the evaluation's epoch base (first kernel of a phase)
+__device__ __forceinline__ void lb_advance_base(unsigned* base) {
+  if (base) *base += LB_EPOCH_STRIDE;
+}
 
 // draw this CTA's tile (thread 0 only); the last ticket resets the counter
 __device__ __forceinline__ unsigned lb_ticket(const LookbackState& S, unsigned ntiles) {
@@ -35,7 +50,7 @@ template <int NW>
 __device__ __forceinline__ void lb_prefix(const LookbackState& S, unsigned tile,
                                           const long long (&agg)[NW], long long (&excl)[NW],
                                           bool head = false) {
-  const unsigned tag = S.epoch << 2;
+  const unsigned tag = lb_tag_epoch(S.epoch, S.base) << 2;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int w = 0; w < NW; ++w) excl[w] = 0;
@@ -101,7 +116,8 @@ namespace fmm {
 struct LookbackPacked {
   unsigned long long* word;   // [ntiles]
   unsigned* ticket;
-  unsigned epoch;             // nonzero, < 2^30
+  unsigned epoch;             // launch index within the evaluation (see LookbackState)
+  const unsigned* base;
 };
 
 __device__ __forceinline__ unsigned lb_ticket(const LookbackPacked& S, unsigned ntiles) {
@@ -120,21 +136,22 @@ __device__ __forceinline__ unsigned long long lb_pack(unsigned epoch, unsigned s
 __device__ __forceinline__ unsigned lb_prefix_packed(const LookbackPacked& S, unsigned tile,
                                                      unsigned agg, bool head) {
   const int lane = threadIdx.x & 31;
+  const unsigned ep = lb_tag_epoch(S.epoch, S.base);
   if (tile == 0 || head) {
-    if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 2u, agg));
+    if (lane == 0) atomicExch(S.word + tile, lb_pack(ep, 2u, agg));
     __syncwarp();
     return 0;
   }
-  if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 1u, agg));
+  if (lane == 0) atomicExch(S.word + tile, lb_pack(ep, 1u, agg));
   unsigned excl = 0;
   long long top = (long long)tile - 1;
   while (true) {
     const long long p = top - lane;
-    unsigned long long v = lb_pack(S.epoch, 2u, 0u);   // lanes past tile 0: terminator
+    unsigned long long v = lb_pack(ep, 2u, 0u);   // lanes past tile 0: terminator
     if (p >= 0) {
       do {
         v = *(volatile unsigned long long*)(S.word + p);
-      } while ((unsigned)(v >> 34) != S.epoch || ((v >> 32) & 3u) == 0);
+      } while ((unsigned)(v >> 34) != ep || ((v >> 32) & 3u) == 0);
     }
     const unsigned st = (unsigned)(v >> 32) & 3u;
     const unsigned inc = __ballot_sync(0xffffffffu, st == 2u);
@@ -146,7 +163,7 @@ __device__ __forceinline__ unsigned lb_prefix_packed(const LookbackPacked& S, un
     if (inc) break;
     top -= 32;
   }
-  if (lane == 0) atomicExch(S.word + tile, lb_pack(S.epoch, 2u, excl + agg));
+  if (lane == 0) atomicExch(S.word + tile, lb_pack(ep, 2u, excl + agg));
   __syncwarp();
   return excl;
 }

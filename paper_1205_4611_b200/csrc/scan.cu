@@ -2,6 +2,7 @@
 // Used for every CSR offset array (interaction lists) -- integer only, so the
 // result is exact and independent of scheduling.
 #include "engine.h"
+#include "lookback.cuh"
 
 namespace fmm {
 
@@ -87,12 +88,31 @@ scan_tiles(const int* __restrict__ in, int* __restrict__ out, long long n,
   }
 }
 
+__global__ void k_lb_advance(unsigned* base) {
+  pdl_enter();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *base += LB_EPOCH_STRIDE;
+}
+
 __global__ void write_base_total(int* out, const int* base_ptr) {
   pdl_enter();
   out[0] = base_ptr ? *base_ptr : 0;
 }
 
 }  // namespace
+
+unsigned* lb_base_prepare(DBuf& buf, bool& ready, cudaStream_t st) {
+  if (!ready) {
+    buf.reserve(64);
+    FMM_CUDA(cudaMemsetAsync(buf.p, 0, 64, st));
+    ready = true;
+  }
+  return buf.as<unsigned>();
+}
+
+void lb_advance(unsigned* base, cudaStream_t st) {
+  note_launch();
+  launch(k_lb_advance, 1, 32, 0, st, base);
+}
 
 void scan_exclusive(const int* in, int* out, int64_t n, DBuf& tmp, cudaStream_t st,
                     const int* base) {

@@ -804,7 +804,8 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   // first use (the bounding box when evaluation points are separate)
   bool inputs_waited = false;
   auto wait_inputs = [&] {
-    if (T.inputs_ready && !inputs_waited) FMM_CUDA(cudaStreamWaitEvent(st, T.inputs_ready, 0));
+    if (T.inputs_ready && !inputs_waited && !capture_cut(ACT_WAIT_INPUTS))
+      FMM_CUDA(cudaStreamWaitEvent(st, T.inputs_ready, 0));
     inputs_waited = true;
   };
   if (!T.aliased) wait_inputs();
@@ -899,6 +900,8 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
     const int2 *X0 = T.X0.as<int2>(), *X1 = T.X1.as<int2>(), *Y0 = T.Y0.as<int2>(),
                *Y1 = T.Y1.as<int2>();
     // look-back state of the fused step kernel (grow-only, epoch-tagged)
+    T.lb_epoch = 0;
+    lb_advance(lb_base_prepare(T.lb_base, T.lb_base_ready, st), st);
     if (T.lb_tiles < maxtiles + 1) {
       T.lb_vals.reserve(sizeof(unsigned long long) * (maxtiles + 1));
       T.lb_ticket.reserve(sizeof(unsigned) * 4);
@@ -910,10 +913,9 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       const int nt = P.tile_count[s];
       const int* tseg = P.d_tile_seg.as<int>() + P.tile_base[s];
       const int* tstart = P.d_tile_start.as<int>() + P.tile_base[s];
-      T.lb_epoch = (T.lb_epoch + 1) & 0x3fffffffu;
-      if (T.lb_epoch == 0) T.lb_epoch = 1;
+      ++T.lb_epoch;
       const LookbackPacked lbs{T.lb_vals.as<unsigned long long>(), T.lb_ticket.as<unsigned>(),
-                               T.lb_epoch};
+                               T.lb_epoch, T.lb_base.as<unsigned>()};
       note_launch();
       launch(k_part_step, nt, PART_THREADS, 0, st, a, s, tseg, tstart, T.X0.as<int2>(),
                                                T.X1.as<int2>(), T.Y0.as<int2>(), T.Y1.as<int2>(),
