@@ -39,6 +39,20 @@ constexpr int CL_MAXM = 16;     // ballot masks cached per target (512 candidate
 #ifndef CL_SPLIT_MIN
 #define CL_SPLIT_MIN 1024       // parents per level from which the split classify runs
 #endif
+#ifndef CL_HEAVY_MIN
+#define CL_HEAVY_MIN 64         // strong-list length from which a parent counts as heavy
+#endif
+#ifndef CL_HEAVY_RATIO
+#define CL_HEAVY_RATIO 4        // ... and only if it exceeds this multiple of the mean
+#endif
+// load-balanced chunked predicate/fill kernels unless FMM2D_CL_CHUNKED=0
+bool cl_chunked() {
+  static bool v = [] {
+    const char* e = getenv("FMM2D_CL_CHUNKED");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 // split classify (predicates, then look-back + fill) unless FMM2D_CL_SPLIT=0
 bool cl_split() {
   static bool v = [] {
@@ -62,7 +76,7 @@ __global__ void __launch_bounds__(CL_WARPS * 32)
 k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
            const int* __restrict__ ps_idx, int* so, int* sidx, long long scap, int* woff,
            int* widx, int* wtgt, long long wcap, LookbackState lbs, unsigned ntiles,
-           long long P0, long long P1, long long tb, long long te, DevStatus* st) {
+           long long P0, long long P1, long long tb, long long te, int* maxs, DevStatus* st) {
   pdl_enter();
   __shared__ unsigned s_mask[CL_WARPS][CL_PPW][4][CL_MAXM];
   __shared__ int s_cnt[CL_WARPS][CL_PPW][4][2];
@@ -115,11 +129,14 @@ k_classify(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
       }
     }
     if (lane == 0) {
+      int mx = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         s_cnt[w][u][j][0] = nw[j];
         s_cnt[w][u][j][1] = ns[j];
+        mx = max(mx, ns[j]);
       }
+      if (mx) atomicMax(maxs, mx);      // longest strong list of the level (cl_heavy)
     }
   }
   __syncthreads();
@@ -242,11 +259,10 @@ __device__ __forceinline__ long long cl_wbase(const int* ps_off, long long P, lo
   return (P - P0) + (4ll * (ps_off[P] - ps_off[P0])) / 32;
 }
 
-__global__ void __launch_bounds__(256)
-k_classify_pred(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
-                const int* __restrict__ ps_idx, long long P0, long long P1, long long tb,
-                long long te, int2* cnt, unsigned* masks, long long mplane, DevStatus* st) {
-  pdl_enter();
+__device__ __forceinline__ void classify_pred_parents(
+    int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
+    const int* __restrict__ ps_idx, long long P0, long long P1, long long tb, long long te,
+    int2* cnt, unsigned* masks, long long mplane, DevStatus* st) {
   const int lane = threadIdx.x & 31;
   const long long lb = level_base(l);
   const bool dead = lists_overflowed(st);
@@ -298,6 +314,197 @@ k_classify_pred(int l, LevelGeo geo, double theta, const int* __restrict__ ps_of
   }
 }
 
+// Load-balanced split classify (default for the large levels).  The unit of
+// work is a 32-candidate CHUNK of one parent's candidate list (chunk ids are
+// the mask-word ids cl_wbase above: parent P owns ids [wbase(P), wbase(P+1))
+// and uses the first ceil(4 n_P / 32)), and every warp takes a contiguous
+// range of chunk ids.  A parent with thousands of candidates (clustered
+// inputs: weak lists up to 2894) is then spread over many warps instead of
+// serialising one warp, which bounded the old per-parent kernels' tail.
+// Counts are integer atomics per target (exact, order independent); the fill
+// recovers each chunk's in-list position from the popcounts of the parent's
+// earlier mask words.
+__device__ __forceinline__ long long cl_chunks_total(const int* ps_off, long long P0,
+                                                     long long P1) {
+  return cl_wbase(ps_off, P1, P0);
+}
+// the parent owning chunk id c: largest P in [P0, P1) with wbase(P) <= c
+// (whole warp, 32-ary search)
+__device__ __forceinline__ long long cl_parent_of(const int* ps_off, long long P0, long long P1,
+                                                  long long c) {
+  const int lane = threadIdx.x & 31;
+  long long lo = P0, hi = P1;
+  while (hi - lo > 1) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long probe = lo + (long long)lane * step;
+    const bool ok = probe < hi && cl_wbase(ps_off, probe, P0) <= c;
+    const unsigned b = __ballot_sync(0xffffffffu, ok);
+    const int last = 31 - __clz(b);                 // lane 0 (probe = lo) is always ok
+    lo = lo + (long long)last * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void classify_pred_chunks(
+    int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
+    const int* __restrict__ ps_idx, long long P0, long long P1, long long tb, long long te,
+    int2* cnt, unsigned* masks, long long mplane, DevStatus* st) {
+  if (lists_overflowed(st)) return;
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(l);
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long C = cl_chunks_total(ps_off, P0, P1);
+  const long long per = (C + nwarps - 1) / nwarps;
+  const long long c_begin = wid * per, c_end = min(C, c_begin + per);
+  if (c_begin >= c_end) return;
+  long long P = cl_parent_of(ps_off, P0, P1, c_begin);
+  long long wb = cl_wbase(ps_off, P, P0), wnext = cl_wbase(ps_off, P + 1, P0);
+  int a0 = ps_off[P], ncand = 4 * (ps_off[P + 1] - a0);
+  double rt[4], xt[4], yt[4];
+  bool own[4];
+  auto load_targets = [&]() {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      own[j] = 4 * P + j >= tb && 4 * P + j < te;
+      const long long gb = lb + 4 * P + j;
+      rt[j] = geo.r[gb];
+      xt[j] = geo.cx[gb];
+      yt[j] = geo.cy[gb];
+    }
+  };
+  load_targets();
+  int nw[4] = {0, 0, 0, 0}, ns[4] = {0, 0, 0, 0};
+  auto flush = [&]() {
+    if (lane < 4) {
+      int w = 0, s2 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j == lane) { w = nw[j]; s2 = ns[j]; }
+      if (w) atomicAdd(&cnt[4 * (P - P0) + lane].x, w);
+      if (s2) atomicAdd(&cnt[4 * (P - P0) + lane].y, s2);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nw[j] = ns[j] = 0;
+  };
+  for (long long c = c_begin; c < c_end; ++c) {
+    if (c >= wnext) {                       // next parent(s): chunk ids are monotone in P
+      flush();
+      do {
+        ++P;
+        wb = wnext;
+        wnext = cl_wbase(ps_off, P + 1, P0);
+      } while (c >= wnext);
+      a0 = ps_off[P];
+      ncand = 4 * (ps_off[P + 1] - a0);
+      load_targets();
+    }
+    const int c0 = 32 * (int)(c - wb);
+    if (c0 >= ncand) continue;              // unused id of this parent
+    const int cc = c0 + lane;
+    const bool valid = cc < ncand;
+    const long long gc = lb + (valid ? 4 * ps_idx[a0 + (cc >> 2)] + (cc & 3) : 0);
+    const double xc = geo.cx[gc], yc = geo.cy[gc], rc = geo.r[gc];
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    unsigned mk = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!own[j]) continue;                // warp-uniform
+      const bool far = valid && well_separated_dz(rt[j], rc, xt[j] - xc, yt[j] - yc, theta);
+      const unsigned m = __ballot_sync(0xffffffffu, far);
+      if (lane == j) mk = m;
+      nw[j] += __popc(m);
+      ns[j] += __popc(vm & ~m);
+    }
+    if (lane < 4 && own[lane & 3]) masks[lane * mplane + c] = mk;
+  }
+  flush();
+}
+
+__device__ __forceinline__ void classify_fill_chunks(
+    int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx,
+    const int* __restrict__ so, int* sidx, long long scap, const int* __restrict__ woff,
+    int* widx, int* wtgt, long long wcap, long long P0, long long P1, long long tb, long long te,
+    const unsigned* __restrict__ masks, long long mplane, DevStatus* st) {
+  if (lists_overflowed(st)) return;
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(l);
+  const unsigned below = (1u << lane) - 1u;
+  if (woff[lb + 4 * P1] > wcap || so[4 * P1] > scap) {   // level totals past capacity
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 1);
+    }
+    return;
+  }
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long C = cl_chunks_total(ps_off, P0, P1);
+  const long long per = (C + nwarps - 1) / nwarps;
+  const long long c_begin = wid * per, c_end = min(C, c_begin + per);
+  if (c_begin >= c_end) return;
+  long long P = cl_parent_of(ps_off, P0, P1, c_begin);
+  long long wb = 0, wnext = cl_wbase(ps_off, P, P0);
+  int a0 = 0, ncand = 0;
+  bool own[4] = {false, false, false, false};
+  long long wpos[4], spos[4];
+  bool first = true;
+  for (long long c = c_begin; c < c_end; ++c) {
+    if (c >= wnext || first) {              // (re)enter a parent: list bases + earlier chunks
+      if (!first) ++P;
+      while (c >= cl_wbase(ps_off, P + 1, P0)) ++P;
+      wb = cl_wbase(ps_off, P, P0);
+      wnext = cl_wbase(ps_off, P + 1, P0);
+      a0 = ps_off[P];
+      ncand = 4 * (ps_off[P + 1] - a0);
+      const int wl = lane < 4 ? woff[lb + 4 * P + lane] : 0;
+      const int sl = lane < 4 ? so[4 * P + lane] : 0;
+      // far entries of the parent's chunks before c (warp-parallel popcounts)
+      const long long kc = c - wb;
+      int far[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        own[j] = 4 * P + j >= tb && 4 * P + j < te;
+        if (!own[j]) continue;
+        int f = 0;
+        for (long long k = lane; k < kc; k += 32) f += __popc(masks[j * mplane + wb + k]);
+#pragma unroll
+        for (int d = 16; d; d >>= 1) f += __shfl_xor_sync(0xffffffffu, f, d);
+        far[j] = f;
+      }
+      const int before = (int)min(32 * kc, (long long)ncand);   // candidates before chunk c
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        wpos[j] = __shfl_sync(0xffffffffu, wl, j) + far[j];
+        spos[j] = __shfl_sync(0xffffffffu, sl, j) + (before - far[j]);
+      }
+      first = false;
+    }
+    const int c0 = 32 * (int)(c - wb);
+    if (c0 >= ncand) continue;
+    const int cc = c0 + lane;
+    const bool valid = cc < ncand;
+    const int cand = valid ? 4 * ps_idx[a0 + (cc >> 2)] + (cc & 3) : 0;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned mine = lane < 4 && own[lane & 3] ? masks[lane * mplane + c] : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!own[j]) continue;
+      const unsigned m = __shfl_sync(0xffffffffu, mine, j);
+      const unsigned sm = vm & ~m;
+      if ((m >> lane) & 1u) {
+        const long long q = wpos[j] + __popc(m & below);
+        widx[q] = (int)(lb + cand);
+        wtgt[q] = (int)(lb + 4 * P + j);
+      }
+      if ((sm >> lane) & 1u) sidx[spos[j] + __popc(sm & below)] = cand;
+      wpos[j] += __popc(m);
+      spos[j] += __popc(sm);
+    }
+  }
+}
+
 // Exclusive scan of NC per-entry counters (entry stride CS ints) into the
 // CSR offset arrays out[k][0..n] (+ *base for counter 0; the total also to
 // *tot_extra).  Large tiles (SCAN_TILE entries) keep the look-back chain short;
@@ -310,8 +517,8 @@ struct ScanOut {
 };
 template <int NC, int CS>
 __global__ void __launch_bounds__(SCAN_THREADS)
-k_scan_counts(const int* __restrict__ cnt, long long n, ScanOut o, LookbackState lbs,
-              unsigned ntiles, DevStatus* st) {
+k_scan_counts(const int* cnt, long long n, ScanOut o, LookbackState lbs,
+              unsigned ntiles, int* maxs, DevStatus* st) {
   pdl_enter();
   __shared__ long long s_w[SCAN_THREADS / 32][NC];
   __shared__ long long s_excl[NC];
@@ -333,6 +540,15 @@ k_scan_counts(const int* __restrict__ cnt, long long n, ScanOut o, LookbackState
       v[q][k] = (i0 + q < n && !dead) ? cnt[(i0 + q) * CS + k] : 0;
       tsum[k] += v[q][k];
     }
+
+  if (maxs && NC > 1) {                 // longest strong list (counter 1), for cl_heavy
+    int mx = 0;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) mx = max(mx, v[q][NC > 1 ? 1 : 0]);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    if (lane == 0 && mx) atomicMax(maxs, mx);
+  }
   long long incl[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
@@ -380,13 +596,11 @@ k_scan_counts(const int* __restrict__ cnt, long long n, ScanOut o, LookbackState
 // k_classify_fill: one warp per parent (grid-stride, no look-back): the
 // offsets come from the scan, the compacted lists from the stored masks
 // (ascending candidate order, as before).
-__global__ void __launch_bounds__(256)
-k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx,
-                const int* __restrict__ so, int* sidx, long long scap, const int* __restrict__ woff,
-                int* widx, int* wtgt, long long wcap, long long P0, long long P1, long long tb,
-                long long te, const unsigned* __restrict__ masks, long long mplane,
-                DevStatus* st) {
-  pdl_enter();
+__device__ __forceinline__ void classify_fill_parents(
+    int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx,
+    const int* __restrict__ so, int* sidx, long long scap, const int* __restrict__ woff,
+    int* widx, int* wtgt, long long wcap, long long P0, long long P1, long long tb, long long te,
+    const unsigned* __restrict__ masks, long long mplane, DevStatus* st) {
   if (lists_overflowed(st)) return;
   const int lane = threadIdx.x & 31;
   const long long lb = level_base(l);
@@ -442,6 +656,51 @@ k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ p
       }
     }
   }
+}
+
+// Which body runs a split level: the chunked (load-balanced) one when some
+// parent's strong list is far longer than the mean -- clustered inputs -- and
+// the warp-per-parent one otherwise (fewer dependent loads per chunk: faster
+// on uniform inputs).  maxs = the longest strong list among the parents
+// (recorded by the previous level's count pass); decided on the device so
+// the choice needs no host round trip and replays inside a CUDA graph.
+__device__ __forceinline__ bool cl_heavy(const int* ps_off, long long P0, long long P1,
+                                         const int* maxs) {
+  const long long tot = ps_off[P1] - ps_off[P0];
+  const long long mx = *maxs;
+  return mx > CL_HEAVY_MIN && mx * (P1 - P0) > CL_HEAVY_RATIO * tot;
+}
+
+__global__ void __launch_bounds__(256, 3)   // keep the per-parent body's occupancy
+k_classify_pred(int l, LevelGeo geo, double theta, const int* __restrict__ ps_off,
+                const int* __restrict__ ps_idx, long long P0, long long P1, long long tb,
+                long long te, int2* cnt, unsigned* masks, long long mplane, const int* maxs,
+                DevStatus* st) {
+  pdl_enter();
+  if (cl_heavy(ps_off, P0, P1, maxs))
+    classify_pred_chunks(l, geo, theta, ps_off, ps_idx, P0, P1, tb, te, cnt, masks, mplane, st);
+  else
+    classify_pred_parents(l, geo, theta, ps_off, ps_idx, P0, P1, tb, te, cnt, masks, mplane, st);
+}
+
+__global__ void __launch_bounds__(256, 5)
+k_classify_fill(int l, const int* __restrict__ ps_off, const int* __restrict__ ps_idx,
+                const int* __restrict__ so, int* sidx, long long scap, const int* __restrict__ woff,
+                int* widx, int* wtgt, long long wcap, long long P0, long long P1, long long tb,
+                long long te, const unsigned* __restrict__ masks, long long mplane,
+                const int* maxs, int2* cnt, DevStatus* st) {
+  pdl_enter();
+  // the scan has consumed the counters: zero them for the next level's atomics
+  // (the chunked predicate body accumulates into them; no memset per level)
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 4 * (P1 - P0);
+       i += (long long)gridDim.x * blockDim.x)
+    cnt[i] = make_int2(0, 0);
+  if (cl_heavy(ps_off, P0, P1, maxs))
+    classify_fill_chunks(l, ps_off, ps_idx, so, sidx, scap, woff, widx, wtgt, wcap, P0, P1, tb,
+                         te, masks, mplane, st);
+  else
+    classify_fill_parents(l, ps_off, ps_idx, so, sidx, scap, woff, widx, wtgt, wcap, P0, P1,
+                          tb, te, masks, mplane, st);
 }
 
 // reclassify_finest (connectivity.py:71-96) in one pass: a warp walks CL_TPW
@@ -583,11 +842,10 @@ k_reclassify(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
 // 32-source chunk (word base of target b: (b - tb) + (s_off[b] - s_off[tb]) /
 // 32) and the three counts; k_reclassify_fill publishes its tile's counts to
 // the look-back first and then writes the three compacted lists.
-__global__ void __launch_bounds__(256)
-k_reclassify_pred(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
-                  const int* __restrict__ s_idx, long long tb, long long te, int4* cnt,
-                  unsigned* masks, long long mplane, DevStatus* st) {
-  pdl_enter();
+__device__ __forceinline__ void reclassify_pred_targets(
+    int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
+    const int* __restrict__ s_idx, long long tb, long long te, int4* cnt, unsigned* masks,
+    long long mplane, DevStatus* st) {
   const int lane = threadIdx.x & 31;
   const long long lb = level_base(L);
   const bool dead = lists_overflowed(st);
@@ -625,22 +883,11 @@ k_reclassify_pred(int L, LevelGeo geo, double theta, const int* __restrict__ s_o
   }
 }
 
-__global__ void __launch_bounds__(256)
-k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx,
-                  const int* __restrict__ o_p2p, int* i_p2p, long long cap_p2p,
-                  const int* __restrict__ o_p2l, int* i_p2l, long long cap_p2l,
-                  const int* __restrict__ o_m2p, int* i_m2p, long long cap_m2p, long long tb,
-                  long long te, const unsigned* __restrict__ masks, long long mplane,
-                  DevStatus* st) {
-  pdl_enter();
-  if (lists_overflowed(st)) return;
-  if (o_p2p[te] > cap_p2p || o_p2l[te] > cap_p2l || o_m2p[te] > cap_m2p) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      atomicOr(&st->flags, ST_OVERFLOW);
-      atomicOr(&st->overflow_where, 2);
-    }
-    return;
-  }
+__device__ __forceinline__ void reclassify_fill_targets(
+    const int* __restrict__ s_off, const int* __restrict__ s_idx, const int* __restrict__ o_p2p,
+    int* i_p2p, const int* __restrict__ o_p2l, int* i_p2l, const int* __restrict__ o_m2p,
+    int* i_m2p, long long tb, long long te, const unsigned* __restrict__ masks,
+    long long mplane) {
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -667,6 +914,187 @@ k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx,
 }
 
 // off[i] for i outside the written window [lo, hi]: off[lo] before, off[hi] after
+// chunked (load-balanced) reclassify: chunk ids over targets as in the
+// per-target form (target b owns [(b - tb) + (s_off[b] - s_off[tb]) / 32, ...));
+// counts by integer atomics, fill positions from earlier chunks' popcounts
+__device__ __forceinline__ long long rc_wbase(const int* s_off, long long b, long long tb) {
+  return (b - tb) + (s_off[b] - s_off[tb]) / 32;
+}
+__device__ __forceinline__ long long rc_target_of(const int* s_off, long long tb, long long te,
+                                                  long long c) {
+  const int lane = threadIdx.x & 31;
+  long long lo = tb, hi = te;
+  while (hi - lo > 1) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long probe = lo + (long long)lane * step;
+    const bool ok = probe < hi && rc_wbase(s_off, probe, tb) <= c;
+    const unsigned bm = __ballot_sync(0xffffffffu, ok);
+    lo = lo + (long long)(31 - __clz(bm)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void reclassify_pred_chunks(
+    int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
+    const int* __restrict__ s_idx, long long tb, long long te, int4* cnt, unsigned* masks,
+    long long mplane, DevStatus* st) {
+  if (lists_overflowed(st)) return;
+  const int lane = threadIdx.x & 31;
+  const long long lb = level_base(L);
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long C = rc_wbase(s_off, te, tb);
+  const long long per = (C + nwarps - 1) / nwarps;
+  const long long c_begin = wid * per, c_end = min(C, c_begin + per);
+  if (c_begin >= c_end) return;
+  long long b = rc_target_of(s_off, tb, te, c_begin);
+  long long wb = rc_wbase(s_off, b, tb), wnext = rc_wbase(s_off, b + 1, tb);
+  int a0 = s_off[b], a1 = s_off[b + 1];
+  double rt = geo.r[lb + b], xt = geo.cx[lb + b], yt = geo.cy[lb + b];
+  int n0 = 0, n1 = 0, n2 = 0;
+  auto flush = [&]() {
+    if (lane == 0) {
+      if (n0) atomicAdd(&cnt[b - tb].x, n0);
+      if (n1) atomicAdd(&cnt[b - tb].y, n1);
+      if (n2) atomicAdd(&cnt[b - tb].z, n2);
+    }
+    n0 = n1 = n2 = 0;
+  };
+  for (long long c = c_begin; c < c_end; ++c) {
+    if (c >= wnext) {
+      flush();
+      do {
+        ++b;
+        wb = wnext;
+        wnext = rc_wbase(s_off, b + 1, tb);
+      } while (c >= wnext);
+      a0 = s_off[b];
+      a1 = s_off[b + 1];
+      rt = geo.r[lb + b];
+      xt = geo.cx[lb + b];
+      yt = geo.cy[lb + b];
+    }
+    const int c0 = a0 + 32 * (int)(c - wb);
+    if (c0 >= a1) continue;
+    const int cc = c0 + lane;
+    const bool valid = cc < a1;
+    int kind = 0;
+    if (valid) {
+      const int src = s_idx[cc];
+      const double rs = geo.r[lb + src];
+      const bool sw = well_separated_swapped_dz(rt, rs, xt - geo.cx[lb + src],
+                                                yt - geo.cy[lb + src], theta);
+      const bool moved = sw && src != b && rs != rt;
+      kind = moved ? (rs > rt ? 1 : 2) : 0;
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned ml = __ballot_sync(0xffffffffu, kind == 1);
+    const unsigned mm = __ballot_sync(0xffffffffu, kind == 2);
+    if (lane == 0) masks[c] = ml;
+    if (lane == 1) masks[mplane + c] = mm;
+    n0 += __popc(vm & ~(ml | mm));
+    n1 += __popc(ml);
+    n2 += __popc(mm);
+  }
+  flush();
+}
+
+__device__ __forceinline__ void reclassify_fill_chunks(
+    const int* __restrict__ s_off, const int* __restrict__ s_idx, const int* __restrict__ o_p2p,
+    int* i_p2p, const int* __restrict__ o_p2l, int* i_p2l, const int* __restrict__ o_m2p,
+    int* i_m2p, long long tb, long long te, const unsigned* __restrict__ masks,
+    long long mplane) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long C = rc_wbase(s_off, te, tb);
+  const long long per = (C + nwarps - 1) / nwarps;
+  const long long c_begin = wid * per, c_end = min(C, c_begin + per);
+  if (c_begin >= c_end) return;
+  long long b = rc_target_of(s_off, tb, te, c_begin);
+  long long wb = 0, wnext = -1;
+  int a0 = 0, a1 = 0;
+  long long q0 = 0, q1 = 0, q2 = 0;
+  for (long long c = c_begin; c < c_end; ++c) {
+    if (c >= wnext) {                       // (re)enter a target: bases + earlier chunks
+      if (wnext >= 0) ++b;
+      while (c >= rc_wbase(s_off, b + 1, tb)) ++b;
+      wb = rc_wbase(s_off, b, tb);
+      wnext = rc_wbase(s_off, b + 1, tb);
+      a0 = s_off[b];
+      a1 = s_off[b + 1];
+      const long long kc = c - wb;
+      int fl = 0, fm = 0;
+      for (long long k = lane; k < kc; k += 32) {
+        fl += __popc(masks[wb + k]);
+        fm += __popc(masks[mplane + wb + k]);
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) {
+        fl += __shfl_xor_sync(0xffffffffu, fl, d);
+        fm += __shfl_xor_sync(0xffffffffu, fm, d);
+      }
+      const int before = (int)min(32 * kc, (long long)(a1 - a0));
+      q0 = o_p2p[b] + (before - fl - fm);
+      q1 = o_p2l[b] + fl;
+      q2 = o_m2p[b] + fm;
+    }
+    const int c0 = a0 + 32 * (int)(c - wb);
+    if (c0 >= a1) continue;
+    const int cc = c0 + lane;
+    const int src = cc < a1 ? s_idx[cc] : 0;
+    const unsigned vm = __ballot_sync(0xffffffffu, cc < a1);
+    const unsigned ml = masks[c], mm = masks[mplane + c];
+    const unsigned mp = vm & ~(ml | mm);
+    if ((mp >> lane) & 1u) i_p2p[q0 + __popc(mp & below)] = src;
+    if ((ml >> lane) & 1u) i_p2l[q1 + __popc(ml & below)] = src;
+    if ((mm >> lane) & 1u) i_m2p[q2 + __popc(mm & below)] = src;
+    q0 += __popc(mp);
+    q1 += __popc(ml);
+    q2 += __popc(mm);
+  }
+}
+
+__global__ void __launch_bounds__(256, 4)
+k_reclassify_pred(int L, LevelGeo geo, double theta, const int* __restrict__ s_off,
+                  const int* __restrict__ s_idx, long long tb, long long te, int4* cnt,
+                  unsigned* masks, long long mplane, const int* maxs, DevStatus* st) {
+  pdl_enter();
+  if (cl_heavy(s_off, tb, te, maxs))
+    reclassify_pred_chunks(L, geo, theta, s_off, s_idx, tb, te, cnt, masks, mplane, st);
+  else
+    reclassify_pred_targets(L, geo, theta, s_off, s_idx, tb, te, cnt, masks, mplane, st);
+}
+
+__global__ void __launch_bounds__(256, 7)
+k_reclassify_fill(const int* __restrict__ s_off, const int* __restrict__ s_idx,
+                  const int* __restrict__ o_p2p, int* i_p2p, long long cap_p2p,
+                  const int* __restrict__ o_p2l, int* i_p2l, long long cap_p2l,
+                  const int* __restrict__ o_m2p, int* i_m2p, long long cap_m2p, long long tb,
+                  long long te, const unsigned* __restrict__ masks, long long mplane,
+                  const int* maxs, int4* cnt, DevStatus* st) {
+  pdl_enter();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < te - tb;
+       i += (long long)gridDim.x * blockDim.x)
+    cnt[i] = make_int4(0, 0, 0, 0);
+  if (lists_overflowed(st)) return;
+  if (o_p2p[te] > cap_p2p || o_p2l[te] > cap_p2l || o_m2p[te] > cap_m2p) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicOr(&st->flags, ST_OVERFLOW);
+      atomicOr(&st->overflow_where, 2);
+    }
+    return;
+  }
+  if (cl_heavy(s_off, tb, te, maxs))
+    reclassify_fill_chunks(s_off, s_idx, o_p2p, i_p2p, o_p2l, i_p2l, o_m2p, i_m2p, tb, te, masks,
+                           mplane);
+  else
+    reclassify_fill_targets(s_off, s_idx, o_p2p, i_p2p, o_p2l, i_p2l, o_m2p, i_m2p, tb, te,
+                            masks, mplane);
+}
+
 __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
   pdl_enter();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -675,8 +1103,11 @@ __global__ void k_csr_pad(int* off, long long n, long long lo, long long hi) {
   else if (i > hi) off[i] = off[hi];
 }
 
-__global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx, unsigned* lb_base) {
+__global__ void k_root_lists(int* weak_off, int* s_off, int* s_idx, unsigned* lb_base,
+                             int* lvl_max, int nlvl) {
   pdl_enter();
+  for (int i = threadIdx.x; i < nlvl; i += blockDim.x) lvl_max[i] = 0;
+  if (threadIdx.x) return;
   lb_advance_base(lb_base);   // this evaluation's look-back epoch base (lookback.cuh)
   weak_off[0] = 0;
   weak_off[1] = 0;     // the root has no far field (connectivity.py:106)
@@ -782,10 +1213,18 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
   const long long rplane = nleaf + Ls.cap_strong / 32 + 4;          // reclassify planes (2)
   if (cl_split()) {
     Ls.cl_cnt.reserve(sizeof(int4) * (nleaf + 4));
+    if (Ls.cl_cnt_zeroed != (long long)Ls.cl_cnt.bytes) {   // fresh buffer: zero once; each
+      FMM_CUDA(cudaMemsetAsync(Ls.cl_cnt.p, 0, Ls.cl_cnt.bytes, st));   // scan re-zeroes it
+      Ls.cl_cnt_zeroed = (long long)Ls.cl_cnt.bytes;
+    }
     Ls.cl_mask.reserve(sizeof(unsigned) * std::max(4 * mplane, 2 * rplane));
   }
+  // longest strong list per level (cl_heavy); slot L+1 is a permanent zero
+  Ls.lvl_max.reserve(sizeof(int) * (L + 2));
+  int* lvl_max = Ls.lvl_max.as<int>();
   note_launch();
-  launch(k_root_lists, 1, 1, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>(), lb_base);
+  launch(k_root_lists, 1, 32, 0, st, woff, Ls.s_off[0].as<int>(), Ls.s_idx[0].as<int>(), lb_base,
+         lvl_max, L + 2);
   int cur = 0;
   for (int l = 1; l <= L; ++l) {
     const long long tb = part.lo(l), te = part.hi(l);
@@ -793,23 +1232,25 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     if (cl_split() && P1 - P0 >= CL_SPLIT_MIN) {
       const long long nt = 4 * (P1 - P0);
       const unsigned stiles = (unsigned)((nt + SCAN_TILE - 1) / SCAN_TILE);
-      const unsigned wgrid = std::min(nblk((P1 - P0) * 32, 256), CL_GRID_CAP);
+      // parents' longest strong list (recorded by level l-1); slot L+1 stays 0
+      const int* maxs_prev = cl_chunked() ? lvl_max + (l - 1) : lvl_max + (L + 1);
       note_launch();
-      launch(k_classify_pred, wgrid, 256, 0, st, l, geo, theta, Ls.s_off[cur].as<int>(),
+      launch(k_classify_pred, CL_GRID_CAP, 256, 0, st, l, geo, theta, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), P0, P1, tb, te, Ls.cl_cnt.as<int2>(),
-             Ls.cl_mask.as<unsigned>(), mplane, dstat);
+             Ls.cl_mask.as<unsigned>(), mplane, maxs_prev, dstat);
       const ScanOut so{{woff + level_base(l) + 4 * P0, Ls.s_off[1 - cur].as<int>() + 4 * P0,
                         nullptr},
                        woff + level_base(l), woff + level_base(l + 1)};
       note_launch();
       launch(k_scan_counts<2, 2>, stiles, SCAN_THREADS, 0, st,
              reinterpret_cast<const int*>(Ls.cl_cnt.as<int2>()), nt, so, lbstate(), stiles,
-             dstat);
+             lvl_max + l, dstat);
       note_launch();
-      launch(k_classify_fill, wgrid, 256, 0, st, l, Ls.s_off[cur].as<int>(),
+      launch(k_classify_fill, CL_GRID_CAP, 256, 0, st, l, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(),
              Ls.cap_strong, woff, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, P0,
-             P1, tb, te, Ls.cl_mask.as<unsigned>(), mplane, dstat);
+             P1, tb, te, Ls.cl_mask.as<unsigned>(), mplane, maxs_prev, Ls.cl_cnt.as<int2>(),
+             dstat);
     } else {
       const unsigned ntiles = (unsigned)((P1 - P0 + CL_WARPS * CL_PPW - 1) / (CL_WARPS * CL_PPW));
       note_launch();
@@ -817,7 +1258,7 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
           l, geo, theta, Ls.s_off[cur].as<int>(), Ls.s_idx[cur].as<int>(),
           Ls.s_off[1 - cur].as<int>(), Ls.s_idx[1 - cur].as<int>(), Ls.cap_strong, woff,
           Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), Ls.cap_weak, lbstate(), ntiles, P0, P1,
-          tb, te, dstat);
+          tb, te, lvl_max + l, dstat);
     }
     cur = 1 - cur;
   }
@@ -826,23 +1267,24 @@ void run_connectivity(const TreeState& T, ListState& Ls, double theta, DevStatus
     const unsigned ntiles = (unsigned)((te - tb + CL_WARPS * CL_TPW - 1) / (CL_WARPS * CL_TPW));
     if (cl_split() && te - tb >= 4 * CL_SPLIT_MIN) {
       const unsigned stiles = (unsigned)((te - tb + SCAN_TILE - 1) / SCAN_TILE);
-      const unsigned wgrid = std::min(nblk((te - tb) * 32, 256), CL_GRID_CAP);
+      const int* maxs_fin = cl_chunked() ? lvl_max + L : lvl_max + (L + 1);
       note_launch();
-      launch(k_reclassify_pred, wgrid, 256, 0, st, L, geo, theta, Ls.s_off[cur].as<int>(),
+      launch(k_reclassify_pred, CL_GRID_CAP, 256, 0, st, L, geo, theta, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), tb, te, Ls.cl_cnt.as<int4>(), Ls.cl_mask.as<unsigned>(),
-             rplane, dstat);
+             rplane, maxs_fin, dstat);
       const ScanOut so{{Ls.p2p_off.as<int>() + tb, Ls.p2l_off.as<int>() + tb,
                         Ls.m2p_off.as<int>() + tb},
                        nullptr, nullptr};
       note_launch();
       launch(k_scan_counts<3, 4>, stiles, SCAN_THREADS, 0, st,
              reinterpret_cast<const int*>(Ls.cl_cnt.as<int4>()), te - tb, so, lbstate(), stiles,
-             dstat);
+             nullptr, dstat);
       note_launch();
-      launch(k_reclassify_fill, wgrid, 256, 0, st, Ls.s_off[cur].as<int>(),
+      launch(k_reclassify_fill, CL_GRID_CAP, 256, 0, st, Ls.s_off[cur].as<int>(),
              Ls.s_idx[cur].as<int>(), Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(), Ls.cap_p2p,
              Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), Ls.cap_p2l, Ls.m2p_off.as<int>(),
-             Ls.m2p_idx.as<int>(), Ls.cap_m2p, tb, te, Ls.cl_mask.as<unsigned>(), rplane, dstat);
+             Ls.m2p_idx.as<int>(), Ls.cap_m2p, tb, te, Ls.cl_mask.as<unsigned>(), rplane,
+             maxs_fin, Ls.cl_cnt.as<int4>(), dstat);
     } else {
       note_launch();
       launch(k_reclassify, ntiles, CL_WARPS * 32, 0, st,

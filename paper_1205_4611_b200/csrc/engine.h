@@ -156,6 +156,8 @@ struct ListState {
   DBuf s_off[2], s_idx[2];           // strong lists ping-pong (level-local ids)
   DBuf lb_flags, lb_vals, lb_ticket;  // single-pass look-back state of the list kernels
   DBuf cl_cnt, cl_mask;              // split classify: per-target counts, far masks
+  DBuf lvl_max;                      // int[L+2]: longest strong list per level (cl_heavy)
+  long long cl_cnt_zeroed = 0;       // bytes of cl_cnt known to be zero
   long long lb_tiles = 0;
   unsigned lb_epoch = 0;             // launch index within the evaluation
   DBuf lb_base;                      // device epoch base (lookback.cuh)
