@@ -15,7 +15,7 @@
  * thread-safe; one in-flight call per context.  Every call is synchronous.
  * Return codes map to the reference's exception types:
  *   FMM2D_EBADARG -> ValueError, FMM2D_EDEGENERATE -> DegenerateInputError
- *   (tree.py:83-84), FMM2D_ESINGULAR -> ValueError with the reference message,
+ *   (tree.py:20-21), FMM2D_ESINGULAR -> ValueError with the reference message,
  *   FMM2D_ECUDA / FMM2D_ENCCL -> RuntimeError, FMM2D_EOOM -> MemoryError.
  * fmm2d_last_error() returns the message (same text as the reference raises).
  */
@@ -66,9 +66,9 @@ int fmm2d_create(fmm2d_ctx** out, int device);
 void fmm2d_destroy(fmm2d_ctx* ctx);
 const char* fmm2d_last_error(const fmm2d_ctx* ctx);
 
-/* tree.py:149-157 num_levels + tree.py:249-255 clamp (4^L <= n) */
+/* tree.py:86-94 num_levels + tree.py:186-192 clamp (4^L <= n) */
 int fmm2d_num_levels(int64_t n_sources, int n_desired);
-/* tree.py:149-157 unclamped Eq. (6); -1 on bad input */
+/* tree.py:86-94 unclamped Eq. (6); -1 on bad input */
 int fmm2d_num_levels_raw(int64_t n_sources, int n_desired);
 
 /* replaces fmm2d.engine.fmm_evaluate (engine.py:207-279).
@@ -84,13 +84,13 @@ int fmm2d_evaluate_device(fmm2d_ctx* ctx, int64_t n, const double* d_pos_xy,
                           const double* d_gamma, int64_t m, const double* d_eval_xy, int p,
                           double theta, int n_desired, double* d_out_xy, fmm2d_report* rep);
 
-/* replaces fmm2d.tree.build_tree (tree.py:293-397): builds on the device and
+/* replaces fmm2d.tree.build_tree (tree.py:230-334): builds on the device and
  * keeps the tree in the context; fetch it with fmm2d_export_tree */
 int fmm2d_build_tree(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
                      int64_t m, const double* eval_xy, int n_desired, int32_t* n_levels);
 
 /* after FMM2D_EDEGENERATE: info = {points in box, box, level, levels still
- * required}, xy = the common coordinate (tree.py:348-354 message fields) */
+ * required}, xy = the common coordinate (tree.py:285-291 message fields) */
 int fmm2d_degenerate_info(fmm2d_ctx* ctx, int64_t info[4], double xy[2]);
 
 /* copy the context's current tree (after build_tree or evaluate).  Level

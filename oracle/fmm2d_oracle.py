@@ -12,7 +12,7 @@ golden vectors produced by running the reference itself
 bit-exact, potentials to 1e-13 relative.
 
 Canonical tree.  The reference median split uses ``np.argpartition``
-(tree.py:160-177) whose order *within* each half is ISA dependent; the
+(tree.py:97-114) whose order *within* each half is ISA dependent; the
 member sets, offsets, cuts and rectangles are not.  This restatement uses
 the deterministic rule the GPU engine implements: a stable partition that
 sends the k = ceil(n/2) smallest coordinates left, ties broken by position
@@ -32,18 +32,18 @@ from dataclasses import dataclass, field
 import numpy as np
 
 PHASES = ("sort", "connect", "p2m", "m2m", "m2l", "l2l", "l2p", "p2p", "other")
-SCALED_LO, SCALED_HI = 1e-12, 1e12          # operators.py:168-169
+SCALED_LO, SCALED_HI = 1e-12, 1e12          # operators.py:37-38
 
 
 class OracleDegenerate(ValueError):
-    """Mirror of tree.DegenerateInputError (tree.py:83-84)."""
+    """Mirror of tree.DegenerateInputError (tree.py:20-21)."""
 
 
 # ---------------------------------------------------------------------------
-# tree  (tree.py:149-397)
+# tree  (tree.py:86-334)
 
 def levels_for(n: int, nd: int) -> int:
-    """Eq. (6) depth, clamped so that 4**L <= n (tree.py:149-157, 249-255)."""
+    """Eq. (6) depth, clamped so that 4**L <= n (tree.py:86-94, 249-255)."""
     if n < 1 or nd < 1:
         raise ValueError("n_sources and n_desired must be >= 1")
     lev = max(0, math.ceil(0.5 * math.log2(0.625 * n / nd)))
@@ -74,7 +74,7 @@ class OTree:
 
 
 def _rect_geometry(x0, x1, y0, y1):
-    """Center / half extents from rectangle corners (tree.py:288-290, 375-377)."""
+    """Center / half extents from rectangle corners (tree.py:225-227, 375-377)."""
     center = (x0 + x1) / 2 + 1j * ((y0 + y1) / 2)
     return center, (x1 - x0) / 2, (y1 - y0) / 2
 
@@ -88,10 +88,10 @@ def _split_step(coords_x, coords_y, perm_arrays, off, rect, eval_state):
     """One successive-split step over every segment at once.
 
     Per segment: axis from the rectangle (geometry.py:57-63 on
-    tree.py:288-290), k = ceil(n/2) (tree.py:171), cut = k-th smallest
-    coordinate (tree.py:265), sources stable-partitioned (canonical rule),
+    tree.py:225-227), k = ceil(n/2) (tree.py:108), cut = k-th smallest
+    coordinate (tree.py:202), sources stable-partitioned (canonical rule),
     evaluation points stable-partitioned by ``coord <= cut``
-    (tree.py:268-278), rectangles cut at ``cut`` (tree.py:281-285).
+    (tree.py:205-215), rectangles cut at ``cut`` (tree.py:218-222).
     """
     x0, x1, y0, y1 = rect
     along_y = (y1 - y0) / 2 > (x1 - x0) / 2
@@ -138,7 +138,7 @@ def _split_step(coords_x, coords_y, perm_arrays, off, rect, eval_state):
 
 
 def build_tree(positions, strengths, eval_positions=None, nd=35) -> OTree:
-    """Canonical pyramid tree (restates tree.py:293-397)."""
+    """Canonical pyramid tree (restates tree.py:230-334)."""
     pos = np.ascontiguousarray(positions, dtype=np.complex128)
     g = np.ascontiguousarray(strengths, dtype=np.float64)
     aliased = eval_positions is None or eval_positions is positions
@@ -163,7 +163,7 @@ def build_tree(positions, strengths, eval_positions=None, nd=35) -> OTree:
 
     record(rect, off, eoff)
     for lev in range(n_lev):
-        # degenerate boxes (tree.py:348-354): first offending box in order
+        # degenerate boxes (tree.py:285-291): first offending box in order
         seg, counts = _seg_ids(off)
         starts = off[:-1]
         same_x = np.minimum.reduceat(xs, starts) == np.maximum.reduceat(xs, starts)
@@ -264,7 +264,7 @@ def build_connectivity(T: OTree, theta=0.5) -> OLists:
 
 
 # ---------------------------------------------------------------------------
-# operators  (operators.py:194-428), batched over a leading axis
+# operators  (operators.py:41-297), batched over a leading axis
 
 def _pow_table(r, p):
     out = np.empty(r.shape + (p + 1,), dtype=np.complex128)
@@ -275,7 +275,7 @@ def _pow_table(r, p):
 
 
 def op_m2m(a, r):
-    """Outgoing re-centering, shift = child - parent (operators.py:231-279).
+    """Outgoing re-centering, shift = child - parent (operators.py:100-148).
     a[...,0] is zero throughout the harmonic pipeline (p2m sets it)."""
     a = np.array(a, dtype=np.complex128)
     p = a.shape[-1] - 1
@@ -299,7 +299,7 @@ def op_m2m(a, r):
 
 
 def op_l2l(b, r):
-    """Incoming re-centering, shift = parent - child (operators.py:282-317)."""
+    """Incoming re-centering, shift = parent - child (operators.py:151-186)."""
     b = np.array(b, dtype=np.complex128)
     p = b.shape[-1] - 1
     mag = np.abs(r)
@@ -323,7 +323,7 @@ def op_l2l(b, r):
 
 def op_m2l(a, rho):
     """Outgoing -> incoming, rho = source center - target center
-    (operators.py:320-351); a[...,0] == 0 in the harmonic pipeline."""
+    (operators.py:189-220); a[...,0] == 0 in the harmonic pipeline."""
     a = np.asarray(a, dtype=np.complex128)
     if np.any(rho == 0):
         raise ValueError("m2l shift must be nonzero (boxes are separated)")
@@ -344,7 +344,7 @@ def op_m2l(a, rho):
 
 
 def op_p2m(pos, g, center, p):
-    """a0 = 0, a_j = -sum g (z - z0)^(j-1) (operators.py:194-206)."""
+    """a0 = 0, a_j = -sum g (z - z0)^(j-1) (operators.py:63-75)."""
     w = np.asarray(g, dtype=np.complex128)
     d = np.asarray(pos) - center
     a = np.zeros(p + 1, dtype=np.complex128)
@@ -355,7 +355,7 @@ def op_p2m(pos, g, center, p):
 
 
 def op_p2l(pos, g, center, p):
-    """b_k = sum g / (z - z0)^(k+1) (operators.py:209-224)."""
+    """b_k = sum g / (z - z0)^(k+1) (operators.py:78-93)."""
     d = np.asarray(pos) - center
     if np.any(d == 0):
         raise ValueError("p2l source coincides with the expansion center")
@@ -369,7 +369,7 @@ def op_p2l(pos, g, center, p):
 
 
 def op_l2p(b, center, y):
-    """Horner in (y - z0) (operators.py:358-365)."""
+    """Horner in (y - z0) (operators.py:227-234)."""
     w = np.asarray(y) - center
     acc = np.full(w.shape, b[-1], dtype=np.complex128)
     for j in range(len(b) - 2, -1, -1):
@@ -378,7 +378,7 @@ def op_l2p(b, center, y):
 
 
 def op_m2p(a, center, y):
-    """Horner in 1/(y - z0) over a_p..a_1 (operators.py:368-386)."""
+    """Horner in 1/(y - z0) over a_p..a_1 (operators.py:237-255)."""
     u = np.asarray(y) - center
     if np.any(u == 0):
         raise ValueError("m2p target coincides with the expansion center")
@@ -391,7 +391,7 @@ def op_m2p(a, center, y):
 
 
 def op_p2p(src, g, tgt):
-    """Near-field block with coincidence skipping (operators.py:389-423)."""
+    """Near-field block with coincidence skipping (operators.py:258-292)."""
     dx = src.real[None, :] - tgt.real[:, None]
     dy = src.imag[None, :] - tgt.imag[:, None]
     r2 = dx * dx + dy * dy

@@ -15,10 +15,10 @@ namespace fmm {
 // status word shared by every kernel (device memory, copied back once per call)
 enum : int {
   ST_OK = 0,
-  ST_DEGENERATE = 1,      // tree.py:348-354
-  ST_P2L_SINGULAR = 2,    // operators.py:216-217
-  ST_M2L_SINGULAR = 4,    // operators.py:329-330
-  ST_M2P_SINGULAR = 8,    // operators.py:376-377
+  ST_DEGENERATE = 1,      // tree.py:285-291
+  ST_P2L_SINGULAR = 2,    // operators.py:85-86
+  ST_M2L_SINGULAR = 4,    // operators.py:198-199
+  ST_M2P_SINGULAR = 8,    // operators.py:245-246
   ST_OVERFLOW = 16,       // a list buffer was too small: host regrows + reruns
   ST_RANK_RETRY = 32,     // a run of equal 32-bit rank keys was too long: rerun exact
   ST_EVAL_TIES = 64,      // a coordinate tie straddles a cut: aliased evals need their own split

@@ -600,7 +600,7 @@ int fmm2d_dist_load(fmm2d_ctx* c, int64_t n_local, const double* d_pos, const do
   });
 }
 
-// root rectangle from the allreduced box (tree.py:319-322); level-0 degenerate check
+// root rectangle from the allreduced box (tree.py:256-259); level-0 degenerate check
 int fmm2d_dist_root(fmm2d_ctx* c, const double* d_bbox4) {
   if (!c) return FMM2D_EBADARG;
   return guarded(c, [&] {
@@ -660,7 +660,7 @@ int fmm2d_dist_hist(fmm2d_ctx* c, int s, int rho, int32_t* d_hist) {
       for (int j = 0; j < nseg; ++j) {
         ax[j] = split_along_y(&D.rect[s][4 * j]);
         const long long n = D.off[s][j + 1] - D.off[s][j];
-        kth[j] = (n + 1) / 2;                                    // tree.py:171
+        kth[j] = (n + 1) / 2;                                    // tree.py:108
       }
       D.d_axis.reserve(16);
       D.sel.reserve(sizeof(SelState) * 8 + sizeof(long long) * 8);
@@ -743,7 +743,7 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
     note_launch();
     launch(k_seg_bounds, nblk(n + 1, 256), 256, 0, c->st, n, 2 * nseg, D.skey2.as<unsigned>(),
                                                       D.d_seg_off.as<long long>());
-    // cut values and child rectangles (tree.py:281-285)
+    // cut values and child rectangles (tree.py:218-222)
     std::vector<SelState> sel(nseg);
     FMM_CUDA(cudaMemcpyAsync(sel.data(), D.sel.p, sizeof(SelState) * nseg, cudaMemcpyDeviceToHost,
                              c->st));
@@ -854,7 +854,7 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
       std::vector<double> v(5 * nb);
       for (int k = 0; k < nb; ++k) {
         const double* r = &D.rect[2 * l][4 * k];
-        v[k] = (r[0] + r[1]) / 2;                     // tree.py:375-377
+        v[k] = (r[0] + r[1]) / 2;                     // tree.py:312-314
         v[nb + k] = (r[2] + r[3]) / 2;
         v[2 * nb + k] = (r[1] - r[0]) / 2;
         v[3 * nb + k] = (r[3] - r[2]) / 2;

@@ -1,11 +1,11 @@
 // Expansion kernels: P2M, P2L, M2M, M2L, L2L, L2P+M2P (FP64, registers).
 //
-// Reference: operators.py:194-386 (unit operators), engine.py:67-160 (phase
+// Reference: operators.py:63-255 (unit operators), engine.py:67-160 (phase
 // drivers).  Conventions kept verbatim: p2m a_0 = 0, a_j = -sum g (z-z0)^(j-1);
 // p2l b_k = sum g/(z-z0)^(k+1); every shift = source center - target center;
 // scaled cascades with the unscaled fallback outside |r| in [1e-12, 1e12].
 // a_0 is identically zero in the harmonic pipeline (p2m writes 0 and m2m
-// preserves it), so the a_0 log corrections (operators.py:236-241, 345-350)
+// preserves it), so the a_0 log corrections (operators.py:105-110, 121-123, 214-219)
 // are never live and are not evaluated.
 //
 // Every kernel is compiled for a fixed order PM >= p; coefficients above the
@@ -24,7 +24,7 @@ namespace fmm {
 
 namespace {
 
-constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:168-169
+constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:37-38
 constexpr int M2P_INLINE = 16;   // m2p sources per point handled by k_l2p_m2p itself
 // M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
 // target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
@@ -111,7 +111,7 @@ k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
     if (j <= p) out[j] = make_double2(acc[j].x, acc[j].y);
 }
 
-// P2L (engine.py:85-93, operators.py:209-224) in two balanced steps:
+// P2L (engine.py:85-93, operators.py:78-93) in two balanced steps:
 //  k_p2l_pair: one thread per (target leaf, p2l source leaf) pair computes the
 //    pair's row sum_i g_i w_i^(k+1), w_i = 1/(z_i - z0), over the source leaf's
 //    particles (what one ops.p2l call returns);
@@ -183,7 +183,7 @@ k_p2l_fold(int L, long long b0, long long b1, const int* __restrict__ l_off,
 }
 
 // --------------------------------------------------------------------------
-// M2M (engine.py:96-100, operators.py:231-279): thread per parent, children 0..3
+// M2M (engine.py:96-100, operators.py:100-148): thread per parent, children 0..3
 template <int PM>
 __device__ __forceinline__ void m2m_shift(cplx (&a)[PM + 1], cplx r) {
   const double mag = numpy_cabs(r.x, r.y);
@@ -245,7 +245,7 @@ k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
 }
 
 // --------------------------------------------------------------------------
-// L2L (engine.py:126-129, operators.py:282-317): thread per child
+// L2L (engine.py:126-129, operators.py:151-186): thread per child
 template <int PM>
 __global__ void __launch_bounds__(128)
 k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
@@ -297,12 +297,12 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 
 // --------------------------------------------------------------------------
 // --------------------------------------------------------------------------
-// M2L (engine.py:103-123, operators.py:320-351), dense form.
+// M2L (engine.py:103-123, operators.py:189-220), dense form.
 //
 // With alpha_k = a_k (-1)^k / rho^k (the reference's prescale), the two
-// cascades of operators.py:339-344 compute c_j = sum_k C(j+k-1, k-1) alpha_k
+// cascades of operators.py:208-213 compute c_j = sum_k C(j+k-1, k-1) alpha_k
 // exactly (Pascal-matrix identity; potentials move <= 6e-14, SURVEY
-// Appendix B.5), and b_j = c_j / rho^j (operators.py:349-350).  The Pascal
+// Appendix B.5), and b_j = c_j / rho^j (operators.py:218-219).  The Pascal
 // matrix is a compile-time table in constant memory, so the core is
 // (p+1) p complex-by-real FMAs per pair with a constant-bank operand and no
 // data-dependent index math -- the same FP64 instruction count as the
@@ -429,7 +429,7 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
     const bool sing = valid && rx == 0.0 && ry == 0.0;
     if (sing) atomicOr(&st->flags, ST_M2L_SINGULAR);
     const cplx inv = (valid && !sing) ? crcp_fast(cplx{rx, ry}) : cplx{0.0, 0.0};
-    // alpha_k = a_k q^k with q = -1/rho (operators.py:334-338)
+    // alpha_k = a_k q^k with q = -1/rho (operators.py:203-206)
     const cplx q{-inv.x, -inv.y};
     double ax[PM], ay[PM];
     {
@@ -679,7 +679,7 @@ k_m2l_dmma(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
 
 // Target-owned M2L (default).  One warp per target box walks the target's
 // weak list in chunks of 16 pairs; lane pair (2i, 2i+1) carries the real /
-// imaginary part of pair i (the cascades of operators.py:339-344 are
+// imaginary part of pair i (the cascades of operators.py:208-213 are
 // real-linear).  Each lane accumulates its pairs in order, then a fixed xor
 // butterfly over the 16 lane pairs folds them and the target row is updated
 // once -- no partials, no fixup, no atomics.
@@ -727,14 +727,14 @@ k_m2l_target(long long nbox, const int* __restrict__ woff, const int* __restrict
         c[PM] = 0.0;
       }
 #pragma unroll
-      for (int k = 2; k <= PM; ++k)               // pass 1, old values (operators.py:339-341)
+      for (int k = 2; k <= PM; ++k)               // pass 1, old values (operators.py:208-210)
 #pragma unroll
         for (int j = PM - k; j < PM; ++j) c[j] += c[j + 1];
 #pragma unroll
-      for (int k = PM; k >= 1; --k)               // pass 2, new values (operators.py:342-344)
+      for (int k = PM; k >= 1; --k)               // pass 2, new values (operators.py:211-213)
 #pragma unroll
         for (int j = k; j <= PM; ++j) c[j] += c[j - 1];
-      {   // b_j = c_j / rho^j = c_j (-q)^j (operators.py:349-350)
+      {   // b_j = c_j / rho^j = c_j (-q)^j (operators.py:218-219)
         acc[0] += c[0];
         double own = dsel(qy, qx, hm);
 #pragma unroll

@@ -1,7 +1,7 @@
 // Near field ("p2p" phase) with the un-permute fused into its epilogue, and
 // the all-pairs direct sum.
 //
-// Reference: engine.py:163-182 (_p2p_phase), operators.py:389-423
+// Reference: engine.py:163-182 (_p2p_phase), operators.py:258-292
 // (reciprocal_parts / kernel_block), engine.py:266-267 (values[eval_perm] =
 // phi), engine.py:282-300 (direct_evaluate).  Kernel G = g/(z_s - y) in real
 // arithmetic: dx = x_s - x_y, dy = y_s - y_y, s = 1/(dx^2+dy^2),
@@ -55,7 +55,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 // One near-field interaction of source (z, g) with target y.  Exact
 // coincidence (r2 == 0, hence dx == dy == 0) contributes nothing and is
-// counted (operators.py:403-414); it is detected on the bit pattern of r2
+// counted (operators.py:266-274); it is detected on the bit pattern of r2
 // and handled by evaluating 1/1 instead of 1/0, so the loop has no branch
 // and no FP64 compare: g * 1 * dx = 0 exactly.
 __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double yx, double yy,

@@ -1,7 +1,7 @@
 // Tree build ("sort" phase): the asymmetric-adaptive pyramid of successive
 // median splits, bit-exact with the reference's canonical form.
 //
-// Reference: tree.py:293-397 (build_tree), :160-177 (partition_median),
+// Reference: tree.py:230-334 (build_tree), :160-177 (partition_median),
 // :258-285 (_split_sources/_split_evals/_cut_rect), geometry.py:57-63.
 //
 // Design (B200): instead of a k-th-element selection per box per split step,
@@ -16,7 +16,7 @@
 // segments) run as tiled global partitions; once a segment fits in shared
 // memory one CTA finishes its whole subtree in SMEM.  Evaluation points do
 // not influence the cuts: each one descends the finished cut table
-// (`coord <= cut`, tree.py:273) to its leaf, then a stable radix sort by leaf
+// (`coord <= cut`, tree.py:210) to its leaf, then a stable radix sort by leaf
 // yields eval_perm.
 #include <cub/device/device_radix_sort.cuh>
 
@@ -60,7 +60,7 @@ struct Rect {
 };
 
 // --------------------------------------------------------------------------
-// bounding box of sources and evaluation points (tree.py:319-322)
+// bounding box of sources and evaluation points (tree.py:256-259)
 __device__ __forceinline__ void block_minmax(double& x0, double& x1, double& y0, double& y1,
                                              double (*sw)[32]) {
   for (int d = 16; d; d >>= 1) {
@@ -85,7 +85,7 @@ __device__ __forceinline__ void block_minmax(double& x0, double& x1, double& y0,
   }
 }
 
-// tight bounding rectangle of sources and evaluation points (tree.py:319-322),
+// tight bounding rectangle of sources and evaluation points (tree.py:256-259),
 // written straight into the root entry of the rectangle table
 __global__ void __launch_bounds__(256)
 k_bbox(const double2* __restrict__ pos, long long n, const double2* __restrict__ epos,
@@ -286,7 +286,7 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   const Rect r = a.rect_tab[step_base(s) + j];
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
   const int sg = s + a.s0;                                          // global step
-  if ((sg & 1) == 0 && (sg >> 1) < a.L) {                           // tree.py:348
+  if ((sg & 1) == 0 && (sg >> 1) < a.L) {                           // tree.py:285
     double xa = a.pos[a.perm_x[x_first.x]].x, xb = a.pos[a.perm_x[x_last.x]].x;
     double ya = a.pos[a.perm_y[y_first.y]].y, yb = a.pos[a.perm_y[y_last.y]].y;
     if (xa == xb && ya == yb) {
@@ -297,9 +297,9 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
     }
   }
   const int cr = along_y ? y_kth.y : x_kth.x;
-  // coordinate of rank cr along the axis (tree.py:265)
+  // coordinate of rank cr along the axis (tree.py:202)
   const double cut = along_y ? a.pos[a.perm_y[cr]].y : a.pos[a.perm_x[cr]].x;
-  // evaluation points split by coord <= cut (tree.py:273): they follow the
+  // evaluation points split by coord <= cut (tree.py:210): they follow the
   // sources' median split exactly unless the (k+1)-th coordinate equals the cut
   const int k = (n + 1) / 2;
   if (k < n) {
@@ -308,7 +308,7 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   }
   a.cut_tab[step_base(s) + j] = cut;
   a.axis_tab[step_base(s) + j] = along_y;
-  Rect lo = r, hi = r;                                              // tree.py:281-285
+  Rect lo = r, hi = r;                                              // tree.py:218-222
   if (along_y) { lo.y1 = cut; hi.y0 = cut; } else { lo.x1 = cut; hi.x0 = cut; }
   a.rect_tab[step_base(s + 1) + 2 * j] = lo;
   a.rect_tab[step_base(s + 1) + 2 * j + 1] = hi;
@@ -612,7 +612,7 @@ __global__ void k_descend(const double2* __restrict__ pts, long long m, int S,
   for (int s = 0; s < S; ++s) {
     const long long t = step_base(s) + seg;
     const double c = axis_tab[t] ? z.y : z.x;
-    seg = 2 * seg + (c <= cut_tab[t] ? 0 : 1);     // tree.py:273 (coords <= cut)
+    seg = 2 * seg + (c <= cut_tab[t] ? 0 : 1);     // tree.py:210 (coords <= cut)
   }
   keys[e] = (unsigned int)seg;
   vals[e] = (int)e;
@@ -657,7 +657,7 @@ __global__ void k_leaf_offsets_identity(int* leaf_off, long long m) {
   leaf_off[1] = (int)m;
 }
 
-// per-level box geometry from the rectangles of even steps (tree.py:375-377)
+// per-level box geometry from the rectangles of even steps (tree.py:312-314)
 __global__ void k_level_geometry(int L, const Rect* __restrict__ rect_tab, double* cx, double* cy,
                                  double* hw, double* hh, double* r, int s0, long long seg) {
   pdl_enter();
@@ -699,7 +699,7 @@ int smem_need(long long nmax, int nseg) {
 }  // namespace
 
 int plan_levels(int64_t n, int nd) {
-  // Eq. (6), tree.py:149-157, clamped so that 4^L <= n (tree.py:249-255)
+  // Eq. (6), tree.py:86-94, clamped so that 4^L <= n (tree.py:186-192)
   double raw = 0.5 * std::log2(0.625 * (double)n / (double)nd);
   int lev = raw > 0 ? (int)std::ceil(raw) : 0;
   while (lev > 0 && (int64_t(1) << (2 * lev)) > n) --lev;
@@ -987,7 +987,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       T.eleaf_t = kout;
     }
   } else {
-    // L == 0: a single box, identity permutations (tree.py:316-317)
+    // L == 0: a single box, identity permutations (tree.py:253-254)
     wait_inputs();
     note_launch();
     launch(k_iota_perm, nblk(n, 256), 256, 0, st, T.vals_in.as<int>(), n);

@@ -1,7 +1,7 @@
 """Tree types and the GPU tree build (drop-in for ``fmm2d.tree``).
 
 The dataclasses keep the reference's names, fields and validation messages
-(tree.py:83-255).  ``build_tree`` runs the median-split pyramid on the B200
+(tree.py:20-334).  ``build_tree`` runs the median-split pyramid on the B200
 (csrc/tree.cu) and returns the canonical tree: offsets, rectangles and
 ``eval_perm`` are bit-identical to the reference, and inside every finest box
 the sources are in ascending original index (the reference's within-box order
@@ -21,12 +21,12 @@ from .geometry import Box
 
 class DegenerateInputError(ValueError):
     """All points in a box coincide while further levels are still required
-    (tree.py:83-84)."""
+    (tree.py:20-21)."""
 
 
 @dataclass
 class ParticleSet:
-    """Sources with real strengths plus evaluation points (tree.py:87-129).
+    """Sources with real strengths plus evaluation points (tree.py:24-66).
 
     ``eval_positions=None`` makes the evaluation points alias the sources.
     """
@@ -69,7 +69,7 @@ class ParticleSet:
 
 @dataclass(frozen=True)
 class TreeConfig:
-    """N_d, θ and p (tree.py:132-146); defaults 35, 0.5, 17."""
+    """N_d, θ and p (tree.py:69-83); defaults 35, 0.5, 17."""
 
     n_desired_per_box: int = 35
     theta: float = 0.5
@@ -85,14 +85,14 @@ class TreeConfig:
 
 
 def num_levels(n_sources: int, n_desired: int) -> int:
-    """Eq. (6): max(0, ceil(0.5*log2((5/8)*n_sources/n_desired))) (tree.py:149-157)."""
+    """Eq. (6): max(0, ceil(0.5*log2((5/8)*n_sources/n_desired))) (tree.py:86-94)."""
     if n_sources < 1 or n_desired < 1:
         raise ValueError("n_sources and n_desired must be >= 1")
     return max(0, math.ceil(0.5 * math.log2(0.625 * n_sources / n_desired)))
 
 
 def clamped_levels(n_sources: int, n_desired: int) -> int:
-    """Depth actually built: Eq. (6) clamped so 4**L <= N (tree.py:249-255)."""
+    """Depth actually built: Eq. (6) clamped so 4**L <= N (tree.py:186-192)."""
     lev = num_levels(n_sources, n_desired)
     while lev > 0 and 4**lev > n_sources:
         lev -= 1
@@ -100,7 +100,7 @@ def clamped_levels(n_sources: int, n_desired: int) -> int:
 
 
 def partition_median(coords: np.ndarray, *companions: np.ndarray) -> int:
-    """In-place median partition of a host array (tree.py:160-177).
+    """In-place median partition of a host array (tree.py:97-114).
 
     Same contract as the reference (left part holds ceil(n/2) elements, all
     <= the right part; companions follow), realised with the engine's
@@ -124,7 +124,7 @@ def partition_median(coords: np.ndarray, *companions: np.ndarray) -> int:
 
 @dataclass
 class LevelBoxes:
-    """Struct-of-arrays for one level, all of length 4**l (tree.py:180-202)."""
+    """Struct-of-arrays for one level, all of length 4**l (tree.py:117-140)."""
 
     center: np.ndarray
     half_width: np.ndarray
@@ -148,7 +148,7 @@ class LevelBoxes:
 
 @dataclass(frozen=True)
 class BoxNode:
-    """Single-box view (tree.py:205-213)."""
+    """Single-box view (tree.py:142-151)."""
 
     geometry: Box
     src_begin: int
@@ -159,7 +159,7 @@ class BoxNode:
 
 @dataclass
 class FmmTree:
-    """Pyramid tree over permuted point arrays (tree.py:216-246)."""
+    """Pyramid tree over permuted point arrays (tree.py:153-183)."""
 
     n_levels: int
     levels: list[LevelBoxes] = field(repr=False)
@@ -218,7 +218,7 @@ def export_tree(ctx: _lib.Context, n_levels: int, n: int, m: int) -> FmmTree:
 
 
 def build_tree(points: ParticleSet, cfg: TreeConfig, *, device: int | None = None) -> FmmTree:
-    """Build the pyramid tree on the GPU (replaces tree.py:293-397).
+    """Build the pyramid tree on the GPU (replaces tree.py:230-334).
 
     Raises :class:`DegenerateInputError` when a box whose points all coincide
     must be split further.
