@@ -22,6 +22,7 @@ enum : int {
   ST_OVERFLOW = 16,       // a list buffer was too small: host regrows + reruns
   ST_RANK_RETRY = 32,     // a run of equal 32-bit rank keys was too long: rerun exact
   ST_EVAL_TIES = 64,      // a coordinate tie straddles a cut: aliased evals need their own split
+  ST_DUPLICATES = 128,    // (not an error) two sources share a position: P2P counts r2 == 0
 };
 
 struct DevStatus {

@@ -96,6 +96,7 @@ struct TreeState {
   int L = 0;
   bool aliased = true;
   bool exact_keys = false;           // 64-bit rank keys (set after a tie-run overflow)
+  bool dup_checked = false;          // this build's x tie pass raised ST_DUPLICATES if needed
   DBuf pos, g, epos;                 // owned input copies, original order
   const double2* pos_p = nullptr;    // inputs actually used (owned copies or caller's
   const double* g_p = nullptr;       //   device memory), original order
@@ -173,6 +174,7 @@ struct ExpState {
   int p = 0;
   DBuf mult, local;                  // double2[nboxes_total * (p+1)]
   DBuf phi;                          // double2[M] tree order
+  DBuf near;                         // double2[M] tree order: P2P result when overlapped
   DBuf values;                       // double2[M] input order
   DBuf partials, item_flags;         // M2L cross-warp partial sums
   DBuf long_list;                    // leaves with long m2p lists (+ count)
@@ -239,7 +241,11 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
 // values in input order, or (out_base >= 0) tree order starting at point out_base
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part = Part(),
-             long long out_base = -1);
+             long long out_base = -1, bool add_phi = true);
+// values[eval_perm[e]] = phi[e] + near[e]: the far field (L2P/M2P) and the near
+// field computed beside M2L on the side stream (same sums as P2P's own epilogue)
+void run_combine(const TreeState& T, ExpState& E, double2* values, DevStatus* dstat,
+                 cudaStream_t st);
 void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st,
                const Part& part = Part());
 

@@ -14,6 +14,10 @@
 // combined in fixed lane order, so results are deterministic.
 #include "engine.h"
 
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 namespace fmm {
 
 namespace {
@@ -29,6 +33,9 @@ constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
 #endif
 #ifndef P2P_EXACT
 #define P2P_EXACT 0
+#endif
+#ifndef P2P_FAST
+#define P2P_FAST 1
 #endif
 
 
@@ -108,8 +115,37 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
 #endif
 }
 
+// The same interaction without the coincidence test, for evaluations whose
+// only coincident pairs are the points with themselves (aliased evaluation
+// points, no two sources at one position: the tree's x tie pass checked,
+// ST_DUPLICATES clear); the host counts those M skips.  The MUFU seed is taken
+// from max(hi(r2), hi(2^-303)): unchanged for every r2 >= 2^-303, and for
+// r2 == 0 (dx == dy == 0) a finite s ~ 5e91, so g s dx == 0 exactly.  The
+// seed's low word is the (dead) seed input instead of zero: < 2^-20 relative
+// on a ~2^-22 seed, which the cubic step takes below 2^-59.  14 instructions,
+// 10 of them FP64, instead of 17.
+__device__ __forceinline__ void p2p_term_fast(double zx, double zy, double g, double yx,
+                                              double yy, double& bx, double& by) {
+  const double dx = zx - yx, dy = zy - yy;
+  const double r2 = fma(dx, dx, dy * dy);
+  double y;
+  asm("{\n\t.reg .b32 h, q, h2, q2;\n\t.reg .b64 s, t;\n\t"
+      "mov.b64 {q, h}, %1;\n\t"
+      "max.s32 h, h, 0x2d000000;\n\t"
+      "mov.b64 s, {q, h};\n\t"
+      "rcp.approx.ftz.f64 t, s;\n\t"
+      "mov.b64 {q2, h2}, t;\n\t"
+      "mov.b64 %0, {h, h2};\n\t}"
+      : "=d"(y) : "d"(r2));
+  const double e = fma(-r2, y, 1.0);
+  const double gs = g * fma(fma(e, e, e), y, y);
+  bx = fma(gs, dx, bx);
+  by = fma(gs, dy, by);
+}
+
 // sum of the staged sources [j0, j1) on target y into (ax, ay): 4-way
 // unrolled, two accumulator pairs, fixed order
+template <bool FAST>
 __device__ __forceinline__ void p2p_slice(const double2* sp, const double* sg, int j0, int j1,
                                           double2 y, double& ax, double& ay, int& skips) {
   const double2* zp = sp + j0;
@@ -120,14 +156,22 @@ __device__ __forceinline__ void p2p_slice(const double2* sp, const double* sg, i
   for (; j + 4 <= n; j += 4) {
     const double2 z0 = zp[j], z1 = zp[j + 1], z2 = zp[j + 2], z3 = zp[j + 3];
     const double g0 = gp[j], g1 = gp[j + 1], g2 = gp[j + 2], g3 = gp[j + 3];
-    p2p_term(z0.x, z0.y, g0, y.x, y.y, bx0, by0, skips);
-    p2p_term(z1.x, z1.y, g1, y.x, y.y, bx1, by1, skips);
-    p2p_term(z2.x, z2.y, g2, y.x, y.y, bx0, by0, skips);
-    p2p_term(z3.x, z3.y, g3, y.x, y.y, bx1, by1, skips);
+    if (FAST) {
+      p2p_term_fast(z0.x, z0.y, g0, y.x, y.y, bx0, by0);
+      p2p_term_fast(z1.x, z1.y, g1, y.x, y.y, bx1, by1);
+      p2p_term_fast(z2.x, z2.y, g2, y.x, y.y, bx0, by0);
+      p2p_term_fast(z3.x, z3.y, g3, y.x, y.y, bx1, by1);
+    } else {
+      p2p_term(z0.x, z0.y, g0, y.x, y.y, bx0, by0, skips);
+      p2p_term(z1.x, z1.y, g1, y.x, y.y, bx1, by1, skips);
+      p2p_term(z2.x, z2.y, g2, y.x, y.y, bx0, by0, skips);
+      p2p_term(z3.x, z3.y, g3, y.x, y.y, bx1, by1, skips);
+    }
   }
   for (; j < n; ++j) {
     const double2 z = zp[j];
-    p2p_term(z.x, z.y, gp[j], y.x, y.y, bx0, by0, skips);
+    if (FAST) p2p_term_fast(z.x, z.y, gp[j], y.x, y.y, bx0, by0);
+    else p2p_term(z.x, z.y, gp[j], y.x, y.y, bx0, by0, skips);
   }
   ax += bx0 + bx1;
   ay += by0 + by1;
@@ -143,7 +187,7 @@ __device__ __forceinline__ void p2p_slice(const double2* sp, const double* sg, i
 // CONTIGUOUS slice of the staged sources (immediate-offset SMEM reads,
 // 4-way unrolled, two accumulator pairs), then the G partial sums are folded
 // in fixed lane order -- deterministic, no atomics on values.
-template <bool DUAL>
+template <bool DUAL, bool FAST>
 __global__ void __launch_bounds__(P2P_THREADS)
 k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __restrict__ eoff,
       const int* __restrict__ n_off, const int* __restrict__ n_idx,
@@ -162,6 +206,10 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
   double2* sp = s_pos[w];
   double* sg = s_g[w];
   int skips = 0;
+  // FAST: no per-pair coincidence test unless the tree found duplicate
+  // sources; the leaf's points meet only themselves (e1 - e0 skips)
+  const bool fast = FAST && !((*(volatile const int*)&st->flags) & ST_DUPLICATES);
+  if (fast && lane == 0) skips = e1 - e0;
   // DUAL: up to 64 points per pass -- block A (<= 32 points, G lane groups)
   // and, for leaves of 33..64 points, block B (the rest, GB groups) share
   // every staged chunk, so the near sources are staged once per 64 points
@@ -264,10 +312,16 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
 #endif
       cp_async_wait_all();
       __syncwarp();
-      if (active) p2p_slice(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
-      // second block of points (leaves of 33..64 points): same staged chunk
-      if (DUAL && activeB)
-        p2p_slice(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
+      if (fast) {
+        if (active) p2p_slice<true>(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
+        // second block of points (leaves of 33..64 points): same staged chunk
+        if (DUAL && activeB)
+          p2p_slice<true>(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
+      } else {
+        if (active) p2p_slice<false>(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
+        if (DUAL && activeB)
+          p2p_slice<false>(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
+      }
       __syncwarp();
     }
     // fold the G lane groups of every point in fixed order
@@ -298,6 +352,19 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
   }
   for (int d = 16; d; d >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, d);
   if (lane == 0 && skips) atomicAdd(&st->p2p_skips, (unsigned long long)skips);
+}
+
+// far + near field, scattered to input order (the P2P epilogue's sums when
+// P2P ran beside M2L: near[e] = (ax, -ay), so phi + near == (phi.x + ax,
+// phi.y - ay) bit for bit)
+__global__ void k_combine(long long m, const double2* __restrict__ phi,
+                          const double2* __restrict__ near, const int* __restrict__ eval_perm,
+                          double2* values, DevStatus* st) {
+  pdl_enter();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= m || lists_overflowed(st)) return;
+  const double2 f = phi[e], a = near[e];
+  values[eval_perm ? (long long)eval_perm[e] : e] = make_double2(f.x + a.x, f.y + a.y);
 }
 
 // all-pairs direct sum, asymmetric mode: thread per target, SMEM source tiles
@@ -341,18 +408,32 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part,
-             long long out_base) {
+             long long out_base, bool add_phi) {
   const long long b0 = part.lo(T.L), b1 = part.hi(T.L);
   // leaves of more than 32 points (mean evaluation points per leaf): the
   // two-block kernel stages each leaf's near sources once per 64 points; the
-  // one-block kernel keeps 64 registers for the common <= 32-point leaves
+  // one-block kernel keeps fewer registers for the common <= 32-point leaves
   const long long nleaf = 1ll << (2 * T.L);
   const bool dual = (T.m + nleaf - 1) / nleaf > 32;
+  const int* eperm = out_base >= 0 ? nullptr : T.eperm_t;
+  const double2* phi_in = add_phi ? E.phi.as<double2>() : nullptr;
+  // fast interaction loop: aliased evaluation points on a single-GPU tree whose
+  // x tie pass checked for duplicate sources (else the per-pair r2 == 0 test)
+  const bool fast = P2P_FAST && T.aliased && T.dup_checked && part.G == 1;
+  auto kern = dual ? (fast ? k_p2p<true, true> : k_p2p<true, false>)
+                   : (fast ? k_p2p<false, true> : k_p2p<false, false>);
   note_launch();
-  launch(dual ? k_p2p<true> : k_p2p<false>, nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0,
+  launch(kern, nblk((b1 - b0) * 32, P2P_THREADS), P2P_THREADS, 0,
          st, b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(),
-         T.src_pos.as<double2>(), T.src_g.as<double>(), T.epos_t,
-         out_base >= 0 ? nullptr : T.eperm_t, E.phi.as<double2>(), values, out_base, dstat);
+         T.src_pos.as<double2>(), T.src_g.as<double>(), T.epos_t, eperm, phi_in,
+         values, out_base, dstat);
+}
+
+void run_combine(const TreeState& T, ExpState& E, double2* values, DevStatus* dstat,
+                 cudaStream_t st) {
+  note_launch();
+  launch(k_combine, nblk(T.m, 256), 256, 0, st, (long long)T.m, E.phi.as<double2>(),
+         E.near.as<double2>(), T.eperm_t, values, dstat);
 }
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,

@@ -241,6 +241,15 @@ __global__ void k_fix_ties(const unsigned* __restrict__ keys, int* perm,
     perm[i + q] = idx[q];
     emit_rank(o, idx[q], (int)(i + q), n);
   }
+  // x pass: exactly equal x are adjacent now; equal y as well means two
+  // sources coincide, so P2P must test r2 == 0 per pair (ST_DUPLICATES)
+  if (axis == 0) {
+    bool dup = false;
+    for (int q = 1; q < cnt && !dup; ++q)
+      for (int r = q - 1; r >= 0 && crd[r] == crd[q] && !dup; --r)
+        dup = pos[idx[r]].y == pos[idx[q]].y;
+    if (dup) atomicOr(&st->flags, ST_DUPLICATES);
+  }
 }
 
 // inverse permutation: rank of every point along the sorted axis (an
@@ -780,6 +789,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
   const double2* pos = T.pos_p;
   const double2* epos = T.aliased ? pos : T.epos_p;
   const long long nseg_total = step_base(S + 1);
+  T.dup_checked = false;
 
   T.src_pos.reserve(sizeof(double2) * (spec.out0 + n));
   T.src_g.reserve(sizeof(double) * (spec.out0 + n));
@@ -879,6 +889,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
           o = RankOut{nullptr, T.rank_x.as<int>(), T.X0.as<int2>(), T.Y0.as<int2>(),
                       T.xpar0.as<unsigned char>(), T.ypar0.as<unsigned char>()};
         launch(k_fix_ties, nblk(n, 256), 256, 0, st, kout, perm, pos, axis, n, o, dstat);
+        if (axis == 0) T.dup_checked = true;
         continue;
       }
       note_launch();
