@@ -43,8 +43,12 @@ struct DevStatus {
 
 // list buffers overflowed earlier in this stream: every list consumer bails out
 // (the host regrows the buffers and reruns the whole evaluation)
+// (a weak L2 load: the flag is set by earlier grids of the stream, or racily
+// by this one -- either way it only lets a consumer stop early; a volatile
+// load here compiled to LDG.STRONG.SYS, a serialised round trip at kernel start)
+__device__ __forceinline__ int status_flags(const DevStatus* st) { return __ldcg(&st->flags); }
 __device__ __forceinline__ bool lists_overflowed(const DevStatus* st) {
-  return (*(volatile const int*)&st->flags) & ST_OVERFLOW;
+  return status_flags(st) & ST_OVERFLOW;
 }
 
 // Programmatic dependent launch: every engine kernel is launched with the

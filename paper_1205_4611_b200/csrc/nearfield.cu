@@ -199,16 +199,18 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
   __shared__ double s_g[P2P_WARPS][P2P_CHUNK];
   const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (b >= b1 || lists_overflowed(st)) return;
+  if (b >= b1) return;
+  // one round trip for the status word and the leaf's point / near-box ranges
+  const int flags = status_flags(st);
   const int e0 = eoff[b], e1 = eoff[b + 1];
-  if (e0 == e1) return;
   const int q0 = n_off[b], q1 = n_off[b + 1];
+  if ((flags & ST_OVERFLOW) || e0 == e1) return;
   double2* sp = s_pos[w];
   double* sg = s_g[w];
   int skips = 0;
   // FAST: no per-pair coincidence test unless the tree found duplicate
   // sources; the leaf's points meet only themselves (e1 - e0 skips)
-  const bool fast = FAST && !((*(volatile const int*)&st->flags) & ST_DUPLICATES);
+  const bool fast = FAST && !(flags & ST_DUPLICATES);
   if (fast && lane == 0) skips = e1 - e0;
   // DUAL: up to 64 points per pass -- block A (<= 32 points, G lane groups)
   // and, for leaves of 33..64 points, block B (the rest, GB groups) share
@@ -226,6 +228,10 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
     const int ei = lane % ne, grp = active ? lane / ne : 0;
     const double2 y = eval_pos[eb + ei];
     double ax = 0.0, ay = 0.0;
+    // epilogue operands fetched now, landing while the pass computes
+    const bool lead = active && grp == 0;
+    const double2 fA = lead && phi_in ? phi_in[eb + ei] : make_double2(0.0, 0.0);
+    const long long dA = !lead ? 0 : eval_perm ? (long long)eval_perm[eb + ei] : eb + ei - out_base;
     // walk the near boxes 32 at a time; (qb, ib) = next box and offset inside it
     int qb = q0, ib = 0;
     while (qb < q1) {
@@ -330,12 +336,8 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
       const double oy = __shfl_sync(0xffffffffu, ay, lane + k * ne);
       if (grp == 0) { ax += ox; ay += oy; }
     }
-    if (active && grp == 0) {
-      const int e = eb + ei;
-      const double2 f = phi_in ? phi_in[e] : make_double2(0.0, 0.0);
-      // input order (engine.py:266-267), or tree order for distributed ranks
-      values[eval_perm ? (long long)eval_perm[e] : e - out_base] = make_double2(f.x + ax, f.y - ay);
-    }
+    // input order (engine.py:266-267), or tree order for distributed ranks
+    if (lead) values[dA] = make_double2(fA.x + ax, fA.y - ay);
     if (DUAL && neB) {
       for (int k = 1; k < GB; ++k) {
         const double ox = __shfl_sync(0xffffffffu, axB, lane + k * neB);
