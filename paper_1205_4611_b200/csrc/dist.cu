@@ -543,8 +543,10 @@ int fmm2d_dist_setup(fmm2d_ctx* c, int G, int rank, int64_t n_total, int p, doub
       for (long long k = 0; k < nleaf; ++k) mx = std::max(mx, D.off[S][k + 1] - D.off[S][k]);
       D.nmax_leaf = std::max(1ll, mx);
       D.leaf_off.reserve(sizeof(int) * (nleaf + 1));
-      FMM_CUDA(cudaMemcpy(D.leaf_off.p, lo.data(), sizeof(int) * (nleaf + 1),
-                          cudaMemcpyHostToDevice));
+      // on the engine stream (ordered with its kernels); lo lives until the sync
+      FMM_CUDA(cudaMemcpyAsync(D.leaf_off.p, lo.data(), sizeof(int) * (nleaf + 1),
+                               cudaMemcpyHostToDevice, c->st));
+      sync(c);
     }
     D.g0 = D.off[D.part.s0][rank];
     D.n_r = D.off[D.part.s0][rank + 1] - D.g0;
@@ -745,13 +747,29 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
                                                       D.d_seg_off.as<long long>());
     // cut values and child rectangles (tree.py:218-222)
     std::vector<SelState> sel(nseg);
+    std::vector<int> eq_all((size_t)D.part.G * nseg);
     FMM_CUDA(cudaMemcpyAsync(sel.data(), D.sel.p, sizeof(SelState) * nseg, cudaMemcpyDeviceToHost,
                              c->st));
+    FMM_CUDA(cudaMemcpyAsync(eq_all.data(), d_eq_all, sizeof(int) * eq_all.size(),
+                             cudaMemcpyDeviceToHost, c->st));
     D.seg_off.assign(2 * nseg + 1, 0);
     FMM_CUDA(cudaMemcpyAsync(D.seg_off.data(), D.d_seg_off.p, sizeof(long long) * (2 * nseg + 1),
                              cudaMemcpyDeviceToHost, c->st));
     sync(c);
     if (n == 0) std::fill(D.seg_off.begin(), D.seg_off.end(), 0);
+    // the evaluation points (aliasing the sources) follow coord <= cut
+    // (tree.py:210): when more sources equal the cut than the k-th-smallest
+    // quota sends left, the reference's evaluation split differs from the
+    // source split.  sel and eq_all are identical on every rank, so every
+    // rank raises here together (no rank is left waiting in a collective).
+    for (int j = 0; j < nseg; ++j) {
+      long long eq = 0;
+      for (int q = 0; q < D.part.G; ++q) eq += eq_all[(size_t)q * nseg + j];
+      if (eq > (long long)sel[j].k_rem)
+        throw ApiError{FMM2D_EBADARG,
+                       "coordinate ties at a median cut are not supported by the distributed "
+                       "engine (evaluate on one GPU)"};
+    }
     D.rect[s + 1].assign(8 * nseg, 0.0);
     for (int j = 0; j < nseg; ++j) {
       const double* r = &D.rect[s][4 * j];
@@ -849,9 +867,13 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
     T.eoff_t = D.leaf_off.as<int>();
     T.eleaf_t = nullptr;
     // shared (top) levels: geometry from the collectively computed rectangles
+    // (uploaded on the engine stream, ordered before the connectivity kernels;
+    // the staging vectors stay alive until the sync below)
+    std::vector<std::vector<double>> stage;
     for (int l = 0; 2 * l < s0 && l <= L; ++l) {
       const int nb = 1 << (2 * l);
-      std::vector<double> v(5 * nb);
+      stage.emplace_back(5 * nb);
+      std::vector<double>& v = stage.back();
       for (int k = 0; k < nb; ++k) {
         const double* r = &D.rect[2 * l][4 * k];
         v[k] = (r[0] + r[1]) / 2;                     // tree.py:312-314
@@ -863,9 +885,10 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
       const long long gb = level_base(l);
       DBuf* arr[5] = {&T.box_cx, &T.box_cy, &T.box_hw, &T.box_hh, &T.box_r};
       for (int f = 0; f < 5; ++f)
-        FMM_CUDA(cudaMemcpy(arr[f]->as<double>() + gb, v.data() + f * nb, sizeof(double) * nb,
-                            cudaMemcpyHostToDevice));
+        FMM_CUDA(cudaMemcpyAsync(arr[f]->as<double>() + gb, v.data() + f * nb,
+                                 sizeof(double) * nb, cudaMemcpyHostToDevice, c->st));
     }
+    if (!stage.empty()) sync(c);
     *own_boxes = own_count(D);
     c->have_tree = true;
     return FMM2D_OK;

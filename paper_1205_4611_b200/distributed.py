@@ -170,6 +170,34 @@ def top_split_steps(size: int) -> int:
     return s0
 
 
+def _rebuild_error(kind: str, msg: str) -> Exception:
+    from .tree import DegenerateInputError
+    return {"DegenerateInputError": DegenerateInputError, "ValueError": ValueError,
+            "MemoryError": MemoryError}.get(kind, _lib.EngineError)(msg)
+
+
+def _agreed(comm: Comm, fn):
+    """Run a library phase that can fail on some ranks only -- a degenerate box
+    or a median tie inside one rank's subtree, a singular shift among one rank's
+    pairs -- then agree on the outcome: every rank raises the failure of the
+    lowest failing rank (same exception type and message as the single-GPU
+    engine), so no rank is left blocked in the next collective."""
+    err = None
+    try:
+        out = fn()
+    except (ValueError, MemoryError, _lib.EngineError) as e:   # DegenerateInputError is a ValueError
+        err, out = e, None
+    info = [None] * comm.size
+    comm.dist.all_gather_object(info, None if err is None else (type(err).__name__, str(err)),
+                                group=comm.group)
+    for q, e in enumerate(info):
+        if e is not None:
+            if q == comm.rank:
+                raise err
+            raise _rebuild_error(*e)
+    return out
+
+
 def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, index_base: int,
                    cfg: TreeConfig):
     """One rank's part of a distributed evaluation.
@@ -230,13 +258,15 @@ def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, 
     recv = torch.empty((sum(recv_counts), 4), dtype=f64, device=dev)
     comm.all_to_all(recv, send, recv_counts, counts)
     own = np.zeros(1, np.int64)
-    ctx.check(lib.fmm2d_dist_build(h, C.c_void_p(recv.data_ptr()), recv.shape[0], _lib.iptr(own)))
+    _agreed(comm, lambda: ctx.check(lib.fmm2d_dist_build(h, C.c_void_p(recv.data_ptr()),
+                                                         recv.shape[0], _lib.iptr(own))))
     geo = torch.empty(int(own[0]) * 5, dtype=f64, device=dev)
     ctx.check(lib.fmm2d_dist_geom_pack(h, C.c_void_p(geo.data_ptr())))
     geo_all = torch.empty(G * int(own[0]) * 5, dtype=f64, device=dev)
     comm.all_gather(geo_all, geo)
     req = np.zeros(2 * G, np.int64)
-    ctx.check(lib.fmm2d_dist_connect(h, C.c_void_p(geo_all.data_ptr()), _lib.iptr(req)))
+    _agreed(comm, lambda: ctx.check(lib.fmm2d_dist_connect(h, C.c_void_p(geo_all.data_ptr()),
+                                                           _lib.iptr(req))))
 
     def exchange(kind):
         mine = [int(v) for v in req[kind * G:(kind + 1) * G]]
@@ -273,8 +303,8 @@ def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, 
     vals = torch.empty((n_own, 2), dtype=f64, device=dev)
     idx = torch.empty(n_own, dtype=i64, device=dev)
     rep = _lib.Report()
-    ctx.check(lib.fmm2d_dist_downward(h, C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()),
-                                      C.byref(rep)))
+    _agreed(comm, lambda: ctx.check(lib.fmm2d_dist_downward(
+        h, C.c_void_p(vals.data_ptr()), C.c_void_p(idx.data_ptr()), C.byref(rep))))
     return vals, idx, rep
 
 

@@ -64,6 +64,40 @@ def engine_run(spec, out):
                                              for k, v in rep.list_histograms.items()}}))
 
 
+def failure_inputs(case):
+    """Inputs on which one rank (or every rank) must raise: 'degenerate' puts
+    400 of 2000 sources on one point in the top-right corner (a level-2 box of
+    one rank's subtree holds only that point; no top cut falls inside it);
+    'ties' is a 39 x 40 lattice: the first median cut lies inside a column of
+    40 equal x, so the quota sends only part of the column left."""
+    import paper_1205_4611_b200 as F
+    rng = np.random.default_rng(3)
+    if case == "degenerate":
+        z = rng.uniform(0.0, 1.0, 1600) + 1j * rng.uniform(0.0, 1.0, 1600)
+        z = np.concatenate([z, np.full(400, 0.93 + 0.99j)])
+    else:
+        z = (np.arange(39)[:, None] / 39.0 + 1j * np.arange(40)[None, :] / 40.0).ravel()
+    return F.ParticleSet(z, rng.uniform(-1.0, 1.0, z.size))
+
+
+def raise_run(case, out):
+    """Every rank must leave the evaluation with the same exception (none
+    may hang in a collective); rank 0 records all outcomes."""
+    import torch.distributed as dist
+    import paper_1205_4611_b200 as F
+    from paper_1205_4611_b200.distributed import fmm_evaluate_distributed
+    pts = failure_inputs(case)
+    try:
+        fmm_evaluate_distributed(pts, F.TreeConfig(35, 0.5, 12), device=0)
+        res = None
+    except Exception as e:     # noqa: BLE001 -- recorded for the test
+        res = [type(e).__name__, str(e)]
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, res)
+    if int(os.environ["RANK"]) == 0:
+        Path(out).write_text(json.dumps(parts))
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -79,6 +113,8 @@ def main():
     try:
         if mode == "comm":
             comm_checks(out)
+        elif mode.startswith("raise:"):
+            raise_run(mode.split(":")[1], out)
         else:
             engine_run(mode, out)
     finally:

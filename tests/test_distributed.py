@@ -88,3 +88,28 @@ def test_distributed_nccl_single_rank(tmp_path):
     ref, rep = F.fmm_evaluate(pts, F.TreeConfig(35, 0.5, 20), device=0)
     assert np.max(np.abs(d["values"] - ref) / np.abs(ref)) <= 1e-13
     assert json.loads(str(d["report"]))["totals"] == rep.list_totals
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,world,exc", [("degenerate", 2, "DegenerateInputError"),
+                                            ("degenerate", 4, "DegenerateInputError"),
+                                            ("ties", 2, "ValueError")])
+def test_distributed_failures_raise_on_every_rank(tmp_path, case, world, exc):
+    """A failure detected by one rank only (a degenerate box inside its
+    subtree) or by the collective top split (ties at a median cut) ends the
+    evaluation on EVERY rank with the same exception type -- no rank blocks in
+    a collective (dist.cu error agreement).  The single-GPU engine
+    raises the same type on the same inputs (ties: it re-splits instead)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _dist_worker as W
+    import paper_1205_4611_b200 as F
+    out = tmp_path / "raise.json"
+    launch(world, f"raise:{case}", out, 29700 + world + len(case), timeout=300)
+    parts = json.loads(out.read_text())
+    assert all(p is not None and p[0] == exc for p in parts), parts
+    assert len({p[1] for p in parts}) == 1, parts
+    if case == "degenerate":
+        with pytest.raises(F.DegenerateInputError):
+            F.fmm_evaluate(W.failure_inputs(case), F.TreeConfig(35, 0.5, 12), device=0)
+    else:
+        assert "ties" in parts[0][1]
