@@ -287,34 +287,42 @@ struct StepArgs {
   long long seg;            // global index of the local root segment at step s0
 };
 
+// The dependent global reads are issued in two waves instead of a chain of
+// seven: (1) the rectangle and every permutation entry either axis could
+// need, (2) the coordinates of the selected entries -- the ranks are known,
+// only the axis comes from the rectangle.  Every caller waits on this at a
+// barrier or a look-back, so the round trips are the step's critical path.
 __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long long j, int s0,
                                                 int n, int2 x_first, int2 x_last, int2 y_first,
                                                 int2 y_last, int2 x_kth, int2 y_kth, int2 x_next,
                                                 int2 y_next, DevStatus* st, int* cut_rank_out,
                                                 bool* along_y_out) {
-  const Rect r = a.rect_tab[step_base(s) + j];
-  const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
   const int sg = s + a.s0;                                          // global step
-  if ((sg & 1) == 0 && (sg >> 1) < a.L) {                           // tree.py:285
-    double xa = a.pos[a.perm_x[x_first.x]].x, xb = a.pos[a.perm_x[x_last.x]].x;
-    double ya = a.pos[a.perm_y[y_first.y]].y, yb = a.pos[a.perm_y[y_last.y]].y;
-    if (xa == xb && ya == yb) {
-      unsigned long long key = ((unsigned long long)(sg >> 1) << 40) |
-                               (unsigned long long)((a.seg << s) + j);
-      atomicMin(&st->degenerate_key, key);
-      atomicOr(&st->flags, ST_DEGENERATE);
-    }
-  }
+  const bool deg = (sg & 1) == 0 && (sg >> 1) < a.L;                // tree.py:285
+  const int k = (n + 1) / 2;
+  // wave 1
+  const Rect r = a.rect_tab[step_base(s) + j];
+  const int ikx = a.perm_x[x_kth.x], iky = a.perm_y[y_kth.y];
+  const int inx = a.perm_x[x_next.x], iny = a.perm_y[y_next.y];
+  const int ixa = a.perm_x[x_first.x], ixb = a.perm_x[x_last.x];
+  const int iya = a.perm_y[y_first.y], iyb = a.perm_y[y_last.y];
+  const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
+  // wave 2: coordinate of rank cr along the axis (tree.py:202), the next
+  // one, and the four extremes of the degenerate check
+  const double2 pc = a.pos[along_y ? iky : ikx];
+  const double2 pn = a.pos[along_y ? iny : inx];
+  const double2 pxa = a.pos[ixa], pxb = a.pos[ixb], pya = a.pos[iya], pyb = a.pos[iyb];
   const int cr = along_y ? y_kth.y : x_kth.x;
-  // coordinate of rank cr along the axis (tree.py:202)
-  const double cut = along_y ? a.pos[a.perm_y[cr]].y : a.pos[a.perm_x[cr]].x;
+  const double cut = along_y ? pc.y : pc.x;
+  if (deg && pxa.x == pxb.x && pya.y == pyb.y) {
+    unsigned long long key = ((unsigned long long)(sg >> 1) << 40) |
+                             (unsigned long long)((a.seg << s) + j);
+    atomicMin(&st->degenerate_key, key);
+    atomicOr(&st->flags, ST_DEGENERATE);
+  }
   // evaluation points split by coord <= cut (tree.py:210): they follow the
   // sources' median split exactly unless the (k+1)-th coordinate equals the cut
-  const int k = (n + 1) / 2;
-  if (k < n) {
-    const double nxt = along_y ? a.pos[a.perm_y[y_next.y]].y : a.pos[a.perm_x[x_next.x]].x;
-    if (nxt == cut) atomicOr(&st->flags, ST_EVAL_TIES);
-  }
+  if (k < n && (along_y ? pn.y : pn.x) == cut) atomicOr(&st->flags, ST_EVAL_TIES);
   a.cut_tab[step_base(s) + j] = cut;
   a.axis_tab[step_base(s) + j] = along_y;
   Rect lo = r, hi = r;                                              // tree.py:218-222
@@ -360,18 +368,6 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
   const Rect r = a.rect_tab[step_base(s) + j];
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
   const int cr = along_y ? Y[s0 + k - 1].y : X[s0 + k - 1].x;
-  if (head && threadIdx.x == 0) {
-    int cr2;
-    bool ay2;
-    const int kn = k < n ? k : k - 1;
-    prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
-                    Y[s0 + k - 1], X[s0 + kn], Y[s0 + kn], st, &cr2, &ay2);
-    // the copy ordered along the split axis stays put; the other one moves
-    const unsigned char nxp = along_y ? (unsigned char)(1 - xp) : xp;
-    const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
-    xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
-    ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
-  }
   const int2* M = along_y ? X : Y;
   int2* D = along_y ? (xp ? X0 : X1) : (yp ? Y0 : Y1);
   const int tend = min(end, tstart + PART_TILE);
@@ -416,6 +412,21 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
       D[dst] = e[q];
       lp += f[q];
     }
+  }
+  // the segment's first tile writes the next step's tables -- after its own
+  // scatter, off the look-back chain that every later tile of the segment
+  // waits on (the next step reads them after this launch completes)
+  if (head && threadIdx.x == 0) {
+    int cr2;
+    bool ay2;
+    const int kn = k < n ? k : k - 1;
+    prepare_segment(a, s, j, s0, n, X[s0], X[s0 + n - 1], Y[s0], Y[s0 + n - 1], X[s0 + k - 1],
+                    Y[s0 + k - 1], X[s0 + kn], Y[s0 + kn], st, &cr2, &ay2);
+    // the copy ordered along the split axis stays put; the other one moves
+    const unsigned char nxp = along_y ? (unsigned char)(1 - xp) : xp;
+    const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
+    xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
+    ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
   }
 }
 
