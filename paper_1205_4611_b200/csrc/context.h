@@ -81,8 +81,7 @@ struct fmm2d_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;   // upward-pass side stream dependencies
   int* h_hist = nullptr;
   cudaEvent_t ev[10] = {};
-  cudaEvent_t ev_side[5] = {};      // P2M / M2M, then P2P, on the tree's side stream (overlapped)
-  cudaEvent_t ev_lists = nullptr, ev_p2p = nullptr;    // P2P side stream dependencies
+  cudaEvent_t ev_side[5] = {};      // P2M / M2M on the side stream (overlapped)
   std::string err;
   bool have_tree = false, have_lists = false, have_eval = false;
   double theta = 0.5;

@@ -109,7 +109,11 @@ struct TreeState {
     cudaEvent_t fork = nullptr, join = nullptr;
     void ensure() {
       if (s) return;
-      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      // lowest priority: side work (upward pass, coarse M2L) fills the SMs the
+      // latency-bound main-stream kernels leave idle instead of delaying them
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, least);
       cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
     }
@@ -174,7 +178,6 @@ struct ExpState {
   int p = 0;
   DBuf mult, local;                  // double2[nboxes_total * (p+1)]
   DBuf phi;                          // double2[M] tree order
-  DBuf near;                         // double2[M] tree order: P2P result when overlapped
   DBuf values;                       // double2[M] input order
   DBuf partials, item_flags;         // M2L cross-warp partial sums
   DBuf long_list;                    // leaves with long m2p lists (+ count)
@@ -241,11 +244,7 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
 // values in input order, or (out_base >= 0) tree order starting at point out_base
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part = Part(),
-             long long out_base = -1, bool add_phi = true);
-// values[eval_perm[e]] = phi[e] + near[e]: the far field (L2P/M2P) and the near
-// field computed beside M2L on the side stream (same sums as P2P's own epilogue)
-void run_combine(const TreeState& T, ExpState& E, double2* values, DevStatus* dstat,
-                 cudaStream_t st);
+             long long out_base = -1);
 void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t st,
                const Part& part = Part());
 

@@ -363,7 +363,7 @@ struct M2LDenseCfg {
 __device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
                                          unsigned char* item_flags, long long item, int p, int t,
                                          int j, int comp, double v, bool starts_before,
-                                         bool ends_after) {
+                                         bool ends_after, bool set_flags = true) {
   if (!starts_before && !ends_after) {
     double* dst = reinterpret_cast<double*>(local + (long long)t * (p + 1)) + 2 * j + comp;
     *dst += v;
@@ -371,7 +371,7 @@ __device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
   }
   const int slot = starts_before ? 0 : 1;
   reinterpret_cast<double*>(partials + (item * 2 + slot) * (p + 1))[2 * j + comp] = v;
-  if (j == 0 && comp == 0) {
+  if (set_flags && j == 0 && comp == 0) {
     const unsigned f = starts_before ? (ends_after ? 5u : 1u) : 2u;
     atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)), f << (8 * (item & 3)));
   }
@@ -399,10 +399,11 @@ __device__ __forceinline__ void m2l_load_pair(M2LPair<PM>& P, long long i, long 
 
 template <int PM>
 __global__ void __launch_bounds__(M2L_ITEM, M2LDenseCfg<PM>::MINB)
-k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
-            const int* __restrict__ w_tgt, const double* __restrict__ cx,
-            const double* __restrict__ cy, const double2* __restrict__ mult, double2* local,
-            double2* partials, unsigned char* item_flags, int p, DevStatus* st) {
+k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
+            const int* __restrict__ w_src, const int* __restrict__ w_tgt,
+            const double* __restrict__ cx, const double* __restrict__ cy,
+            const double2* __restrict__ mult, double2* local, double2* partials,
+            unsigned char* item_flags, int p, DevStatus* st) {
   pdl_enter();
   static_assert(PM <= 32, "dense M2L is compiled for PM <= 32");
   using Cfg = M2LDenseCfg<PM>;
@@ -412,16 +413,22 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
   __shared__ int s_seg[M2L_ITEM + 1];
   __shared__ int s_nseg;
   __shared__ int s_wcnt[M2L_ITEM / 32];
-  const long long npairs = *total_ptr;
+  // pairs [lo, hi) of the flat list (one range of whole levels: no target
+  // spans its ends); items of M2L_ITEM pairs from lo, numbered from ibase in
+  // the partials / flags arrays (disjoint from any range before lo)
+  const long long lo = lo_ptr ? *lo_ptr : 0, hi = *total_ptr;
+  const long long npairs = hi - lo;
   const long long nitems = (npairs + M2L_ITEM - 1) / M2L_ITEM;
+  const long long ibase = lo ? lo / M2L_ITEM + 1 : 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   M2LPair<PM> P;
-  for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
-    m2l_load_pair<PM>(P, item * M2L_ITEM + tid, npairs, w_src, w_tgt, mult, p);
+  for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const long long i0 = lo + it * M2L_ITEM, item = ibase + it;
+    m2l_load_pair<PM>(P, i0 + tid, hi, w_src, w_tgt, mult, p);
     // targets just before / after the item (segments continuing across items)
-    const int prev_t = item > 0 ? __ldg(w_tgt + item * M2L_ITEM - 1) : -1;
-    const long long nxt = (item + 1) * M2L_ITEM;
-    const int next_t = nxt < npairs ? __ldg(w_tgt + nxt) : -1;
+    const int prev_t = it > 0 ? __ldg(w_tgt + i0 - 1) : -1;
+    const long long nxt = i0 + M2L_ITEM;
+    const int next_t = nxt < hi ? __ldg(w_tgt + nxt) : -1;
     const bool valid = P.t >= 0;
     const int t = P.t;
     const int tt = valid ? t : 0;
@@ -487,12 +494,12 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
 #pragma unroll
       for (int w = 0; w < M2L_ITEM / 32; ++w) tot += s_wcnt[w];
       s_nseg = tot;
-      s_seg[tot] = (int)min((long long)M2L_ITEM, npairs - item * M2L_ITEM);
+      s_seg[tot] = (int)min((long long)M2L_ITEM, npairs - it * M2L_ITEM);
     }
     __syncthreads();
     const int nseg = s_nseg;
     const int R = 2 * (p + 1);
-    const bool first_cont = item > 0 && prev_t == s_t[0];
+    const bool first_cont = it > 0 && prev_t == s_t[0];
     const int nvalid = s_seg[nseg];
     const bool last_cont = nvalid == M2L_ITEM && next_t >= 0 && next_t == s_t[nvalid - 1];
     for (int task = tid; task < nseg * R; task += M2L_ITEM) {
@@ -512,8 +519,14 @@ k_m2l_dense(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       if (q + 1 < q1) a1 += row[q + 1];
       if (q + 2 < q1) a2 += row[q + 2];
       m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, (a0 + a1) + (a2 + a3),
-               sg == 0 && first_cont, sg == nseg - 1 && last_cont);
+               sg == 0 && first_cont, sg == nseg - 1 && last_cont, false);
     }
+    // the item's chain flags as one byte store (no memset, no atomics): 1 head
+    // part in slot 0, 2 tail part in slot 1, 5 the whole item continues a chain
+    if (tid == 0)
+      item_flags[item] = (unsigned char)(nseg == 1 && first_cont && last_cont
+                                             ? 5u
+                                             : (first_cont ? 1u : 0u) | (last_cont ? 2u : 0u));
     __syncthreads();
   }
 }
@@ -765,28 +778,29 @@ k_m2l_target(long long nbox, const int* __restrict__ woff, const int* __restrict
 
 // ordered fold of the partial sums of targets whose pairs span several warp
 // items: one warp per item, lanes over coefficients (coalesced rows)
-__global__ void k_m2l_fixup(const int* __restrict__ total_ptr, const int* __restrict__ w_tgt,
-                            const double2* __restrict__ partials,
+__global__ void k_m2l_fixup(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
+                            const int* __restrict__ w_tgt, const double2* __restrict__ partials,
                             const unsigned char* __restrict__ item_flags, double2* local, int p,
                             int item_pairs, const DevStatus* st) {
   pdl_enter();
   if (lists_overflowed(st)) return;
-  const long long npairs = *total_ptr;
-  const long long nitems = (npairs + item_pairs - 1) / item_pairs;
+  const long long lo = lo_ptr ? *lo_ptr : 0, hi = *total_ptr;   // k_m2l_dense's range
+  const long long nitems = (hi - lo + item_pairs - 1) / item_pairs;
+  const long long ibase = lo ? lo / item_pairs + 1 : 0;
   const int lane = threadIdx.x & 31;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nitems;
        w += nwarps) {
-    if (!(item_flags[w] & 2)) continue;          // chain head: its tail segment continues
-    const int t = w_tgt[w * item_pairs + item_pairs - 1];
+    if (!(item_flags[ibase + w] & 2)) continue;  // chain head: its tail segment continues
+    const int t = w_tgt[lo + w * item_pairs + item_pairs - 1];
     double2* dst = local + (long long)t * (p + 1);
     for (int j = lane; j <= p; j += 32) {
-      double2 s = partials[(w * 2 + 1) * (p + 1) + j];
+      double2 s = partials[((ibase + w) * 2 + 1) * (p + 1) + j];
       for (long long u = w + 1; u < nitems; ++u) {
-        const double2 v = partials[(u * 2 + 0) * (p + 1) + j];
+        const double2 v = partials[((ibase + u) * 2 + 0) * (p + 1) + j];
         s.x += v.x;
         s.y += v.y;
-        if (!(item_flags[u] & 4)) break;
+        if (!(item_flags[ibase + u] & 4)) break;
       }
       const double2 o = dst[j];
       dst[j] = make_double2(o.x + s.x, o.y + s.y);
@@ -972,6 +986,7 @@ struct Launch {
     const int L = T.L;
     if (L == 0) return;
     const int* total = Ls.weak_off.as<int>() + level_base(L + 1);
+    const int* lo = nullptr;      // the kernels take a pair range [lo, total); all pairs here
     if constexpr (PM > 32) {
       launch_target(T, Ls, E, dstat, st);
     } else {
@@ -980,11 +995,11 @@ struct Launch {
         return;
       }
       using Cfg = M2LDenseCfg<PM>;
-      const long long items = (Ls.cap_weak + M2L_ITEM - 1) / M2L_ITEM;
+      const long long items = (Ls.cap_weak + M2L_ITEM - 1) / M2L_ITEM + 2;
       E.partials.reserve(sizeof(double2) * 2 * items * (E.p + 1));
       E.item_flags.reserve(((items + 4) & ~3ll) + 8);
-      FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
       if (m2l_dmma()) {
+        FMM_CUDA(cudaMemsetAsync(E.item_flags.p, 0, ((items + 4) & ~3ll) + 8, st));
         using DC = M2LDmmaCfg<PM>;
         static unsigned attr_dmma = 0;
         ensure_smem_attr(k_m2l_dmma<PM>, DC::SMEM, attr_dmma);
@@ -1002,13 +1017,13 @@ struct Launch {
             std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
         note_launch();
         launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st,
-            total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
+            lo, total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
             T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
             E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
       }
       note_launch();
-      launch(k_m2l_fixup, std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st, 
-          total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
+      launch(k_m2l_fixup, std::max(1u, std::min(4096u, nblk(items * 32, 128))), 128, 0, st,
+          lo, total, Ls.weak_tgt.as<int>(), E.partials.as<double2>(),
           E.item_flags.as<unsigned char>(), E.local.as<double2>(), E.p, M2L_ITEM, dstat);
     }
   }

@@ -17,18 +17,6 @@
 
 #include "context.h"
 
-// FMM2D_P2P_OVERLAP=1 runs P2P on the side stream beside M2L -> L2L ->
-// L2P/M2P (it needs only the tree and the lists) and combines the two fields
-// at the end.  Off by default: both are FP64-bound and share the SMs, so M2L
-// slows by what P2P gains (measured C2 1.357 vs 1.351 ms, C5 10.71 vs 10.41).
-bool p2p_overlap() {
-  static bool v = [] {
-    const char* e = getenv("FMM2D_P2P_OVERLAP");
-    return e && std::string(e) == "1";
-  }();
-  return v;
-}
-
 #ifndef UPWARD_OVERLAP
 #define UPWARD_OVERLAP 1   // P2M + M2M beside the connectivity phase
 #endif
@@ -236,18 +224,11 @@ void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values
     rec_time(c->ev_side[2], T.aux.s);
     FMM_CUDA(cudaEventRecord(c->ev_join, T.aux.s));
   }
+  // (M2L of the coarse levels beside the finest level's connectivity, on the
+  // side stream, was measured: the two compete for the SMs and the step time
+  // stays within +-1 % at C2-C5, so M2L runs once after the lists)
   run_connectivity(T, Ls, theta, dst, c->st);
   rec_time(c->ev[2], c->st);
-  const bool p2p_side = overlap && p2p_overlap();
-  if (p2p_side) {
-    E.near.reserve(sizeof(double2) * T.m);
-    FMM_CUDA(cudaEventRecord(c->ev_lists, c->st));
-    FMM_CUDA(cudaStreamWaitEvent(T.aux.s, c->ev_lists, 0));
-    rec_time(c->ev_side[3], T.aux.s);
-    run_p2p(T, Ls, E, offL, E.near.as<double2>(), dst, T.aux.s, Part(), 0, false);
-    rec_time(c->ev_side[4], T.aux.s);
-    FMM_CUDA(cudaEventRecord(c->ev_p2p, T.aux.s));
-  }
   if (L > 0)
     FMM_CUDA(cudaMemsetAsync(E.local.p, 0, sizeof(double2) * level_base(L) * (p + 1), c->st));
   run_upward(T, Ls, E, offL, dst, c->st, Part(), overlap ? 2 : 0);
@@ -262,12 +243,7 @@ void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values
   run_l2p_m2p(T, Ls, E, dst, c->st);
   rec_time(c->ev[7], c->st);
   // P2P adds into phi and scatters to input order (engine.py:263-267)
-  if (p2p_side) {
-    FMM_CUDA(cudaStreamWaitEvent(c->st, c->ev_p2p, 0));
-    run_combine(T, E, values, dst, c->st);
-  } else {
-    run_p2p(T, Ls, E, offL, values, dst, c->st);
-  }
+  run_p2p(T, Ls, E, offL, values, dst, c->st);
   rec_time(c->ev[8], c->st);
   // the result download starts now, on the copy stream beside the report
   // kernels, instead of after the status round trip (a retry simply rewrites
@@ -445,9 +421,6 @@ int evaluate_impl(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, i
     // device_ms, which stays the end-to-end device interval)
     r.phase_ms[2] = ev_ms(c->ev_side[0], c->ev_side[1]) + ev_ms(c->ev[2], c->ev[3]);
     r.phase_ms[3] = ev_ms(c->ev_side[1], c->ev_side[2]);
-    // P2P beside M2L: its own span on the side stream (combine + join wait
-    // stay inside device_ms)
-    if (p2p_overlap()) r.phase_ms[7] = ev_ms(c->ev_side[3], c->ev_side[4]);
   }
   r.device_ms = ev_ms(c->ev[0], c->ev[8]);
   const auto t_end = std::chrono::steady_clock::now();
@@ -477,7 +450,9 @@ int fmm2d_create(fmm2d_ctx** out, int device) {
   c->device = device;
   int rc = guarded(c, [&] {
     FMM_CUDA(cudaSetDevice(device));
-    FMM_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;
+    FMM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    FMM_CUDA(cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, greatest));
     c->own_st = c->st;
     FMM_CUDA(cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_inputs, cudaEventDisableTiming));
@@ -492,8 +467,6 @@ int fmm2d_create(fmm2d_ctx** out, int device) {
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_d2h, cudaEventDisableTiming));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming));
-    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_p2p, cudaEventDisableTiming));
     FMM_CUDA(cudaMallocHost(&c->h_hist, sizeof(int) * 4 * HIST_BINS));
     return FMM2D_OK;
   });
@@ -521,8 +494,6 @@ void fmm2d_destroy(fmm2d_ctx* c) {
   if (c->ev_d2h) cudaEventDestroy(c->ev_d2h);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->ev_lists) cudaEventDestroy(c->ev_lists);
-  if (c->ev_p2p) cudaEventDestroy(c->ev_p2p);
   if (c->h_status_init) cudaFreeHost(c->h_status_init);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_hist) cudaFreeHost(c->h_hist);

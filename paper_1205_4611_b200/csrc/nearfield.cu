@@ -356,19 +356,6 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
   if (lane == 0 && skips) atomicAdd(&st->p2p_skips, (unsigned long long)skips);
 }
 
-// far + near field, scattered to input order (the P2P epilogue's sums when
-// P2P ran beside M2L: near[e] = (ax, -ay), so phi + near == (phi.x + ax,
-// phi.y - ay) bit for bit)
-__global__ void k_combine(long long m, const double2* __restrict__ phi,
-                          const double2* __restrict__ near, const int* __restrict__ eval_perm,
-                          double2* values, DevStatus* st) {
-  pdl_enter();
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= m || lists_overflowed(st)) return;
-  const double2 f = phi[e], a = near[e];
-  values[eval_perm ? (long long)eval_perm[e] : e] = make_double2(f.x + a.x, f.y + a.y);
-}
-
 // all-pairs direct sum, asymmetric mode: thread per target, SMEM source tiles
 constexpr int DIRECT_TILE = 256;
 
@@ -410,7 +397,7 @@ inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* offL,
              double2* values, DevStatus* dstat, cudaStream_t st, const Part& part,
-             long long out_base, bool add_phi) {
+             long long out_base) {
   const long long b0 = part.lo(T.L), b1 = part.hi(T.L);
   // leaves of more than 32 points (mean evaluation points per leaf): the
   // two-block kernel stages each leaf's near sources once per 64 points; the
@@ -418,7 +405,7 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
   const long long nleaf = 1ll << (2 * T.L);
   const bool dual = (T.m + nleaf - 1) / nleaf > 32;
   const int* eperm = out_base >= 0 ? nullptr : T.eperm_t;
-  const double2* phi_in = add_phi ? E.phi.as<double2>() : nullptr;
+  const double2* phi_in = E.phi.as<double2>();
   // fast interaction loop: aliased evaluation points on a single-GPU tree whose
   // x tie pass checked for duplicate sources (else the per-pair r2 == 0 test)
   const bool fast = P2P_FAST && T.aliased && T.dup_checked && part.G == 1;
@@ -429,13 +416,6 @@ void run_p2p(const TreeState& T, const ListState& Ls, ExpState& E, const int* of
          st, b0, b1, offL, T.eoff_t, Ls.p2p_off.as<int>(), Ls.p2p_idx.as<int>(),
          T.src_pos.as<double2>(), T.src_g.as<double>(), T.epos_t, eperm, phi_in,
          values, out_base, dstat);
-}
-
-void run_combine(const TreeState& T, ExpState& E, double2* values, DevStatus* dstat,
-                 cudaStream_t st) {
-  note_launch();
-  launch(k_combine, nblk(T.m, 256), 256, 0, st, (long long)T.m, E.phi.as<double2>(),
-         E.near.as<double2>(), T.eperm_t, values, dstat);
 }
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
