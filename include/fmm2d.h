@@ -188,7 +188,11 @@ int fmm2d_reclassify_finest(fmm2d_ctx* ctx, int64_t nbox, const double* center_x
  *   for s < log2 G: (s even, s>0: segbox -> [allreduce MIN] -> check_segbox)
  *                   8 x (hist -> [allreduce SUM] -> pick)
  *                   eqcount -> [allgather] -> partition
- *   send_counts -> [all-to-all records] -> build -> geom_pack -> [allgather]
+ *   send_counts -> [all-to-all records]
+ *   (separate evaluation points: load_evals right after load -- the box
+ *    allreduce then covers both -- and eval_route -> [all-to-all] after the
+ *    top split; reference tree.py:205-215 / engine.py:207-279)
+ *   -> build -> geom_pack -> [allgather]
  *   -> connect -> 2 x request exchange [all-to-all ids, pack, all-to-all, unpack]
  *      (particles before upward, multipoles after upward_top)
  *   -> upward -> [allgather top multipoles] -> upward_top -> downward -> end
@@ -197,6 +201,8 @@ int fmm2d_dist_setup(fmm2d_ctx* ctx, int world_size, int rank, int64_t n_total, 
                      double theta, int n_desired, void* stream, int32_t* n_levels);
 int fmm2d_dist_load(fmm2d_ctx* ctx, int64_t n_local, const double* d_pos_xy,
                     const double* d_gamma, int64_t index_base, double* d_bbox4);
+int fmm2d_dist_load_evals(fmm2d_ctx* ctx, int64_t m_total, int64_t m_local,
+                          const double* d_eval_xy, int64_t index_base, double* d_bbox4);
 int fmm2d_dist_root(fmm2d_ctx* ctx, const double* d_bbox4);
 int fmm2d_dist_segbox(fmm2d_ctx* ctx, int step, double* d_box);
 int fmm2d_dist_check_segbox(fmm2d_ctx* ctx, int step, const double* d_box);
@@ -205,7 +211,11 @@ int fmm2d_dist_pick(fmm2d_ctx* ctx, int step, int round, const int32_t* d_hist);
 int fmm2d_dist_eqcount(fmm2d_ctx* ctx, int step, int32_t* d_eq);
 int fmm2d_dist_partition(fmm2d_ctx* ctx, int step, const int32_t* d_eq_all);
 int fmm2d_dist_send_counts(fmm2d_ctx* ctx, int64_t* counts, void** d_records);
+int fmm2d_dist_eval_route(fmm2d_ctx* ctx, int64_t* counts, void** d_records);
+/* d_eval_records / n_eval_records: the evaluation records this rank received
+ * (NULL / 0 when the evaluation points alias the sources) */
 int fmm2d_dist_build(fmm2d_ctx* ctx, const double* d_records, int64_t n_records,
+                     const double* d_eval_records, int64_t n_eval_records,
                      int64_t* owned_boxes);
 int fmm2d_dist_geom_pack(fmm2d_ctx* ctx, double* d_send);
 int fmm2d_dist_connect(fmm2d_ctx* ctx, const double* d_geometry_all, int64_t* request_counts);

@@ -89,6 +89,9 @@ _SIGS = {
                                    C.c_int, C.c_void_p, C.POINTER(C.c_int32)]),
     "fmm2d_dist_load": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_void_p]),
+    "fmm2d_dist_load_evals": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                        C.c_void_p]),
+    "fmm2d_dist_eval_route": (C.c_int, [C.c_void_p, _i64p, C.POINTER(C.c_void_p)]),
     "fmm2d_dist_root": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fmm2d_dist_segbox": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "fmm2d_dist_check_segbox": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
@@ -97,7 +100,8 @@ _SIGS = {
     "fmm2d_dist_eqcount": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "fmm2d_dist_partition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "fmm2d_dist_send_counts": (C.c_int, [C.c_void_p, _i64p, C.POINTER(C.c_void_p)]),
-    "fmm2d_dist_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _i64p]),
+    "fmm2d_dist_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                   _i64p]),
     "fmm2d_dist_geom_pack": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fmm2d_dist_connect": (C.c_int, [C.c_void_p, C.c_void_p, _i64p]),
     "fmm2d_dist_requests": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),

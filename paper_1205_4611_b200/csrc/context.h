@@ -37,6 +37,13 @@ struct DistState {
   DBuf req_ids[2];                             // requests grouped by owner
   long long nmax_leaf = 0;                     // records per leaf in halo messages
   DBuf vals;                                   // owned values, tree order
+  // separate evaluation points: sharded like the sources, routed to the rank
+  // owning their top-split segment (coord <= cut), evaluated there
+  bool separate = false;
+  long long m_total = 0, m_local = 0, m_r = 0;
+  DBuf erec_a, erec_b, loc_epos, loc_eidx, eoff_g, eleaf_g, ecount;
+  std::vector<std::vector<double>> cuts;        // top split: cut per segment, steps 0..s0-1
+  std::vector<std::vector<unsigned char>> axes; // ... and its axis
   cudaEvent_t ev[12] = {};
   long long launches0 = 0;
 };

@@ -67,7 +67,7 @@ __global__ void k_rec_load(long long n, const double2* __restrict__ pos,
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const double2 z = pos[i];
-    rec[i] = Rec{z.x, z.y, g[i], idx_base + i};
+    rec[i] = Rec{z.x, z.y, g ? g[i] : 0.0, idx_base + i};
     x0 = fmin(x0, z.x); x1 = fmax(x1, z.x);
     y0 = fmin(y0, z.y); y1 = fmax(y1, z.y);
   }
@@ -431,6 +431,52 @@ __global__ void k_fill_owned_idx(long long n, const int* __restrict__ perm, long
   if (i < n) out[i] = perm[i];
 }
 
+// separate evaluation points: destination rank = top-split segment reached by
+// coord <= cut (tree.py:210) through the s0 collectively chosen cuts
+// (step s, segment j at table entry 2^s - 1 + j)
+__global__ void k_eval_dest(long long m, const Rec* __restrict__ rec, int s0,
+                            const double* __restrict__ cuts, const unsigned char* __restrict__ axes,
+                            unsigned* key, int* val, int* count) {
+  pdl_enter();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const Rec r = rec[i];
+  int seg = 0;
+  for (int s = 0; s < s0; ++s) {
+    const int t = (1 << s) - 1 + seg;
+    seg = 2 * seg + ((axes[t] ? r.y : r.x) <= cuts[t] ? 0 : 1);
+  }
+  key[i] = (unsigned)seg;
+  val[i] = (int)i;
+  atomicAdd(count + seg, 1);
+}
+
+__global__ void k_erec_unpack(long long m, const Rec* __restrict__ rec, double2* pos, int* idx) {
+  pdl_enter();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const Rec r = rec[i];
+  pos[i] = make_double2(r.x, r.y);
+  idx[i] = (int)r.idx;
+}
+
+// global-size evaluation leaf offsets: the owned leaves [b0, b0 + nl) carry
+// the subtree's local offsets, the others are empty (monotone)
+__global__ void k_eoff_global(long long nleaf, long long b0, long long nl,
+                              const int* __restrict__ loc, int m, int* out) {
+  pdl_enter();
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b > nleaf) return;
+  out[b] = b < b0 ? 0 : (b > b0 + nl ? m : loc[b - b0]);
+}
+
+__global__ void k_add_base(long long m, const unsigned* __restrict__ in, unsigned base,
+                           unsigned* out) {
+  pdl_enter();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) out[i] = in[i] + base;
+}
+
 template <class K, class V>
 void sort_pairs(DBuf& tmp, const K* kin, K* kout, const V* vin, V* vout, long long n, int bits,
                 cudaStream_t st) {
@@ -565,6 +611,10 @@ int fmm2d_dist_setup(fmm2d_ctx* c, int G, int rank, int64_t n_total, int p, doub
     for (auto& e : D.ev)
       if (!e) FMM_CUDA(cudaEventCreate(&e));
     D.active = true;
+    D.separate = false;
+    D.m_total = D.m_local = D.m_r = 0;
+    D.cuts.assign(D.part.s0, {});
+    D.axes.assign(D.part.s0, {});
     c->have_tree = c->have_lists = c->have_eval = false;
     if (n_levels) *n_levels = D.L;
     return FMM2D_OK;
@@ -598,6 +648,83 @@ int fmm2d_dist_load(fmm2d_ctx* c, int64_t n_local, const double* d_pos, const do
     FMM_CUDA(cudaMemcpyAsync(D.d_seg_off.p, D.seg_off.data(), sizeof(long long) * 2,
                              cudaMemcpyHostToDevice, c->st));
     sync(c);
+    return FMM2D_OK;
+  });
+}
+
+// separate evaluation points (call after fmm2d_dist_load, before the bbox
+// allreduce): shard [idx_base, idx_base + m_local) of the M = m_total points
+// -> records; the local box written to d_bbox4 now covers sources and
+// evaluation points (tree.py:256-259)
+int fmm2d_dist_load_evals(fmm2d_ctx* c, int64_t m_total, int64_t m_local, const double* d_epos,
+                          int64_t idx_base, double* d_bbox4) {
+  if (!c) return FMM2D_EBADARG;
+  return guarded(c, [&] {
+    DistState& D = dist(c);
+    if (m_total < 1 || m_local < 0 || m_total > INT32_MAX)
+      throw ApiError{FMM2D_EBADARG, "bad evaluation point count"};
+    D.separate = true;
+    D.m_total = m_total;
+    D.m_local = m_local;
+    D.erec_a.reserve(sizeof(Rec) * std::max<long long>(1, m_local));
+    if (m_local > 0) {
+      note_launch();
+      launch(k_rec_load, std::max(1u, std::min(nblk(m_local, 256), 1184u)), 256, 0, c->st,
+             (long long)m_local, reinterpret_cast<const double2*>(d_epos), (const double*)nullptr,
+             (long long)idx_base, D.erec_a.as<Rec>(), D.bbox.as<unsigned long long>());
+    }
+    note_launch();
+    launch(k_bbox_out, 1, 32, 0, c->st, D.bbox.as<unsigned long long>(), d_bbox4);
+    return FMM2D_OK;
+  });
+}
+
+// after the top split: every local evaluation point's destination rank
+// (coord <= cut through the s0 top cuts), records grouped by destination in
+// original order; counts (host int64[G]) and the grouped records
+int fmm2d_dist_eval_route(fmm2d_ctx* c, int64_t* counts, void** d_records) {
+  if (!c) return FMM2D_EBADARG;
+  return guarded(c, [&] {
+    DistState& D = dist(c);
+    const int G = D.part.G, s0 = D.part.s0;
+    if (!D.separate) throw ApiError{FMM2D_EBADARG, "no separate evaluation points loaded"};
+    const long long m = D.m_local;
+    std::vector<double> cut(std::max(1, G - 1));
+    std::vector<unsigned char> ax(std::max(1, G - 1));
+    for (int s = 0; s < s0; ++s) {
+      if ((int)D.cuts[s].size() != (1 << s)) throw ApiError{FMM2D_EBADARG, "top split incomplete"};
+      for (int j = 0; j < (1 << s); ++j) {
+        cut[(1 << s) - 1 + j] = D.cuts[s][j];
+        ax[(1 << s) - 1 + j] = D.axes[s][j];
+      }
+    }
+    D.ecount.reserve(sizeof(int) * G + sizeof(double) * 64 + 64);
+    int* dcount = D.ecount.as<int>();
+    double* dcut = reinterpret_cast<double*>(D.ecount.as<char>() + ((sizeof(int) * G + 15) & ~15ull));
+    unsigned char* dax = reinterpret_cast<unsigned char*>(dcut + 32);
+    FMM_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int) * G, c->st));
+    FMM_CUDA(cudaMemcpyAsync(dcut, cut.data(), sizeof(double) * cut.size(), cudaMemcpyHostToDevice,
+                             c->st));
+    FMM_CUDA(cudaMemcpyAsync(dax, ax.data(), ax.size(), cudaMemcpyHostToDevice, c->st));
+    std::vector<int> hc(G, 0);
+    if (m > 0) {
+      for (DBuf* b : {&D.skey, &D.skey2}) b->reserve(sizeof(unsigned) * m);
+      for (DBuf* b : {&D.sval, &D.sval2}) b->reserve(sizeof(int) * m);
+      note_launch();
+      launch(k_eval_dest, nblk(m, 256), 256, 0, c->st, m, D.erec_a.as<Rec>(), s0, dcut, dax,
+             D.skey.as<unsigned>(), D.sval.as<int>(), dcount);
+      sort_pairs(D.cub_tmp, D.skey.as<unsigned>(), D.skey2.as<unsigned>(), D.sval.as<int>(),
+                 D.sval2.as<int>(), m, std::max(1, s0), c->st);
+      D.erec_b.reserve(sizeof(Rec) * m);
+      note_launch();
+      launch(k_rec_gather, nblk(m, 256), 256, 0, c->st, m, D.sval2.as<int>(), D.erec_a.as<Rec>(),
+             D.erec_b.as<Rec>());
+      D.erec_a.swap(D.erec_b);
+      FMM_CUDA(cudaMemcpyAsync(hc.data(), dcount, sizeof(int) * G, cudaMemcpyDeviceToHost, c->st));
+    }
+    sync(c);   // (cut / ax are host temporaries of the uploads as well)
+    for (int q = 0; q < G; ++q) counts[q] = hc[q];
+    *d_records = D.erec_a.p;
     return FMM2D_OK;
   });
 }
@@ -762,7 +889,7 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
     // quota sends left, the reference's evaluation split differs from the
     // source split.  sel and eq_all are identical on every rank, so every
     // rank raises here together (no rank is left waiting in a collective).
-    for (int j = 0; j < nseg; ++j) {
+    for (int j = 0; j < nseg && !D.separate; ++j) {
       long long eq = 0;
       for (int q = 0; q < D.part.G; ++q) eq += eq_all[(size_t)q * nseg + j];
       if (eq > (long long)sel[j].k_rem)
@@ -778,6 +905,10 @@ int fmm2d_dist_partition(fmm2d_ctx* c, int s, const int32_t* d_eq_all) {
       const unsigned long long bits = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
       double cut;
       std::memcpy(&cut, &bits, sizeof cut);
+      D.cuts[s].resize(nseg);
+      D.axes[s].resize(nseg);
+      D.cuts[s][j] = cut;
+      D.axes[s][j] = ay;
       double* lo = &D.rect[s + 1][8 * j];
       double* hi = lo + 4;
       for (int q = 0; q < 4; ++q) lo[q] = hi[q] = r[q];
@@ -803,7 +934,8 @@ int fmm2d_dist_send_counts(fmm2d_ctx* c, int64_t* counts, void** d_records) {
 // build the owned subtree from the received records (n_r of them, canonical
 // order) and the owned geometry; returns the owned-box count per rank (the
 // geometry allgather is 5 doubles per owned box)
-int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t* own_boxes) {
+int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, const double* d_erecv,
+                     int64_t m_recv, int64_t* own_boxes) {
   if (!c) return FMM2D_EBADARG;
   return guarded(c, [&] {
     DistState& D = dist(c);
@@ -825,12 +957,29 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
     T.pos_p = D.loc_pos.as<double2>();
     T.g_p = D.loc_g.as<double>();
     T.epos_p = nullptr;
+    if (D.separate) {
+      // the evaluation points this rank owns (original order): its subtree's
+      // evaluation split descends the same cut tables (k_descend)
+      D.m_r = m_recv;
+      D.loc_epos.reserve(sizeof(double2) * std::max<long long>(1, m_recv));
+      D.loc_eidx.reserve(sizeof(int) * std::max<long long>(1, m_recv));
+      if (m_recv > 0) {
+        note_launch();
+        launch(k_erec_unpack, nblk(m_recv, 256), 256, 0, c->st, (long long)m_recv,
+               reinterpret_cast<const Rec*>(d_erecv), D.loc_epos.as<double2>(),
+               D.loc_eidx.as<int>());
+      }
+      T.m = m_recv;
+      T.aliased = false;
+      T.epos_p = D.loc_epos.as<double2>();
+    }
     T.inputs_ready = nullptr;
     T.spec = TreeSpec{};
     T.spec.s0 = s0;
     T.spec.seg = rank;
     T.spec.out0 = D.g0;
     T.spec.orig = D.loc_idx.as<int>();
+    T.spec.eorig = D.separate ? D.loc_eidx.as<int>() : nullptr;
     T.spec.root_given = true;
     for (int q = 0; q < 4; ++q) T.spec.root[q] = D.rect[s0][4 * rank + q];
     for (int attempt = 0;; ++attempt) {
@@ -853,7 +1002,7 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
                  (long long)(key & ((1ull << 40) - 1)), (int)(key >> 40), L - (int)(key >> 40));
         throw ApiError{FMM2D_EDEGENERATE, buf};
       }
-      if (fl & ST_EVAL_TIES)
+      if ((fl & ST_EVAL_TIES) && !D.separate)
         throw ApiError{FMM2D_EBADARG,
                        "coordinate ties at a median cut are not supported by the distributed "
                        "engine (evaluate on one GPU)"};
@@ -862,10 +1011,34 @@ int fmm2d_dist_build(fmm2d_ctx* c, const double* d_recv, int64_t n_recv, int64_t
     T.spec = TreeSpec{};
     // every rank sees the whole pyramid through global-size arrays
     T.n = T.m = D.n_total;
-    T.epos_t = T.src_pos.as<double2>();
-    T.eperm_t = T.src_perm.as<int>();
-    T.eoff_t = D.leaf_off.as<int>();
-    T.eleaf_t = nullptr;
+    if (D.separate) {
+      // evaluation arrays stay local (only the owner evaluates them): local tree
+      // order, original indices in eval_perm, global-size leaf offsets and
+      // global leaf ids for the downward kernels
+      const int S = 2 * L - s0;
+      const long long nleaf = 1ll << (2 * L), b0 = (long long)rank << S;
+      T.m = D.m_r;
+      D.eoff_g.reserve(sizeof(int) * (nleaf + 1));
+      note_launch();
+      launch(k_eoff_global, nblk(nleaf + 1, 256), 256, 0, c->st, nleaf, b0, 1ll << S,
+             T.eval_leaf_off.as<int>(), (int)D.m_r, D.eoff_g.as<int>());
+      D.eleaf_g.reserve(sizeof(unsigned) * std::max<long long>(1, D.m_r));
+      if (D.m_r > 0 && T.eleaf_t) {
+        note_launch();
+        launch(k_add_base, nblk(D.m_r, 256), 256, 0, c->st, (long long)D.m_r, T.eleaf_t,
+               (unsigned)b0, D.eleaf_g.as<unsigned>());
+      }
+      T.epos_t = T.eval_pos.as<double2>();
+      T.eperm_t = T.eval_perm.as<int>();
+      T.eoff_t = D.eoff_g.as<int>();
+      T.eleaf_t = D.eleaf_g.as<unsigned>();
+      c->E.phi.reserve(sizeof(double2) * std::max<long long>(D.n_total, D.m_r));
+    } else {
+      T.epos_t = T.src_pos.as<double2>();
+      T.eperm_t = T.src_perm.as<int>();
+      T.eoff_t = D.leaf_off.as<int>();
+      T.eleaf_t = nullptr;
+    }
     // shared (top) levels: geometry from the collectively computed rectangles
     // (uploaded on the engine stream, ordered before the connectivity kernels;
     // the staging vectors stay alive until the sync below)
@@ -1118,13 +1291,19 @@ int fmm2d_dist_downward(fmm2d_ctx* c, double* d_vals, int64_t* d_idx, fmm2d_repo
     record(c, 8);
     run_l2l(T, E, dst, c->st, D.part);
     record(c, 9);
-    run_l2p_m2p(T, Ls, E, dst, c->st, D.g0, D.g0 + D.n_r, D.part.lo(L), D.part.hi(L));
+    // owned evaluation points: the subtree's sources (aliased, tree-order range
+    // [g0, g0 + n_r) of the global arrays) or its separate points (local 0..m_r)
+    const long long e0 = D.separate ? 0 : D.g0, ne = D.separate ? D.m_r : D.n_r;
+    run_l2p_m2p(T, Ls, E, dst, c->st, e0, e0 + ne, D.part.lo(L), D.part.hi(L));
     record(c, 10);
     run_p2p(T, Ls, E, D.leaf_off.as<int>(), reinterpret_cast<double2*>(d_vals), dst, c->st,
-            D.part, D.g0);
-    note_launch();
-    launch(k_fill_owned_idx, nblk(D.n_r, 256), 256, 0, c->st, 
-        D.n_r, T.src_perm.as<int>() + D.g0, reinterpret_cast<long long*>(d_idx));
+            D.part, e0);
+    if (ne > 0) {
+      note_launch();
+      launch(k_fill_owned_idx, nblk(ne, 256), 256, 0, c->st, ne,
+             (D.separate ? T.eval_perm.as<int>() : T.src_perm.as<int>() + D.g0),
+             reinterpret_cast<long long*>(d_idx));
+    }
     record(c, 11);
     run_stats(T, Ls, dst, c->st, D.part);
     fetch_status(c);

@@ -85,6 +85,7 @@ struct TreeSpec {
   long long seg = 0;
   long long out0 = 0;
   const int* orig = nullptr;
+  const int* eorig = nullptr;        // original index of every separate evaluation point
   bool root_given = false;
   double root[4] = {0, 0, 0, 0};     // x0, x1, y0, y1
 };

@@ -1000,7 +1000,7 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       note_launch();
       launch(k_gather_points, nblk(m, 256), 256, 0, st, T.vals_out.as<int>(), m, epos, nullptr,
                                                     T.eval_pos.as<double2>(), nullptr,
-                                                    T.eval_perm.as<int>(), 0ll, nullptr);
+                                                    T.eval_perm.as<int>(), 0ll, spec.eorig);
       note_launch();
       launch(k_leaf_offsets, nblk(m + 1, 256), 256, 0, st, kout, m, 1ll << S, T.eval_leaf_off.as<int>());
       T.epos_t = T.eval_pos.as<double2>();

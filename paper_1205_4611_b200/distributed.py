@@ -199,14 +199,17 @@ def _agreed(comm: Comm, fn):
 
 
 def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, index_base: int,
-                   cfg: TreeConfig):
+                   cfg: TreeConfig, evals=None):
     """One rank's part of a distributed evaluation.
 
     ``d_pos`` (float64 [n_local, 2]) / ``d_gamma`` (float64 [n_local]) are this
     rank's shard of the sources on its GPU, original indices starting at
-    ``index_base`` (shards of consecutive ranks must be consecutive).  Returns
-    (values complex as float64 [n_own, 2] in tree order, their original indices
-    int64 [n_own], library Report of this rank).
+    ``index_base`` (shards of consecutive ranks must be consecutive).
+    ``evals`` = (m_total, d_epos float64 [m_local, 2], eval_index_base) for
+    separate evaluation points, sharded the same way (None: the evaluation
+    points alias the sources).  Returns (values complex as float64 [n_own, 2]
+    in tree order, their original evaluation indices int64 [n_own], library
+    Report of this rank).
     """
     import torch
     lib, h = ctx.lib, ctx.h
@@ -228,6 +231,11 @@ def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, 
     ctx.check(lib.fmm2d_dist_load(h, n_local, C.c_void_p(d_pos.data_ptr()),
                                   C.c_void_p(d_gamma.data_ptr()), int(index_base),
                                   C.c_void_p(bbox.data_ptr())))
+    if evals is not None:
+        m_total, d_epos, e_base = evals
+        ctx.check(lib.fmm2d_dist_load_evals(h, int(m_total), int(d_epos.shape[0]),
+                                            C.c_void_p(d_epos.data_ptr()), int(e_base),
+                                            C.c_void_p(bbox.data_ptr())))
     comm.allreduce(bbox, "min")
     ctx.check(lib.fmm2d_dist_root(h, C.c_void_p(bbox.data_ptr())))
     # top split: s0 exact median steps, collectively
@@ -257,9 +265,24 @@ def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, 
     recv_counts = comm.exchange_counts(counts)
     recv = torch.empty((sum(recv_counts), 4), dtype=f64, device=dev)
     comm.all_to_all(recv, send, recv_counts, counts)
+    erecv = None
+    if evals is not None:
+        # evaluation points to the rank owning their top-split segment (coord <= cut)
+        ecounts = np.zeros(G, np.int64)
+        eptr = C.c_void_p()
+        ctx.check(lib.fmm2d_dist_eval_route(h, _lib.iptr(ecounts), C.byref(eptr)))
+        m_loc = int(ecounts.sum())
+        esend = (torch.as_tensor(DeviceArray(eptr.value or 0, (m_loc, 4), "float64"), device=dev)
+                 if m_loc else torch.empty((0, 4), dtype=f64, device=dev))
+        erecv_counts = comm.exchange_counts(ecounts)
+        erecv = torch.empty((sum(erecv_counts), 4), dtype=f64, device=dev)
+        comm.all_to_all(erecv, esend, erecv_counts, ecounts)
     own = np.zeros(1, np.int64)
+    e_ptr = C.c_void_p(erecv.data_ptr()) if erecv is not None and erecv.shape[0] else None
+    m_recv = 0 if erecv is None else erecv.shape[0]
     _agreed(comm, lambda: ctx.check(lib.fmm2d_dist_build(h, C.c_void_p(recv.data_ptr()),
-                                                         recv.shape[0], _lib.iptr(own))))
+                                                         recv.shape[0], e_ptr, m_recv,
+                                                         _lib.iptr(own))))
     geo = torch.empty(int(own[0]) * 5, dtype=f64, device=dev)
     ctx.check(lib.fmm2d_dist_geom_pack(h, C.c_void_p(geo.data_ptr())))
     geo_all = torch.empty(G * int(own[0]) * 5, dtype=f64, device=dev)
@@ -299,7 +322,7 @@ def evaluate_shard(ctx: _lib.Context, comm: Comm, n_total: int, d_pos, d_gamma, 
     comm.all_gather(top_all, top)
     ctx.check(lib.fmm2d_dist_upward_top(h, C.c_void_p(top_all.data_ptr())))
     keep.append(exchange(0))                             # halo multipoles (M2L, M2P)
-    n_own = recv.shape[0]
+    n_own = recv.shape[0] if erecv is None else erecv.shape[0]
     vals = torch.empty((n_own, 2), dtype=f64, device=dev)
     idx = torch.empty(n_own, dtype=i64, device=dev)
     rep = _lib.Report()
@@ -347,57 +370,89 @@ def fmm_evaluate_distributed(points: ParticleSet, cfg: TreeConfig | None = None,
                              device: int | None = None, gather: bool = True):
     """SPMD drop-in for ``fmm_evaluate`` (engine.py:207-279) across the ranks of
     ``group`` (one GPU each): every rank passes the same point set, uploads its
-    shard, and (``gather=True``) receives all values in input order.
+    shard of the sources (and of separate evaluation points), and
+    (``gather=True``) receives all values in input order.
 
     ``gather=False`` returns ``(values_owned complex128, original_indices)`` of
     the evaluation points this rank owns instead of the full array.
+
+    Aliased evaluation points follow the sources' median splits; when a
+    coordinate tie straddles a cut the reference's evaluation split (coord <=
+    cut, tree.py:205-215) differs from the source split, and -- like the
+    single-GPU engine -- the evaluation reruns with the points handled as
+    separate evaluation points (every rank reruns together: the tie is agreed).
     """
     import torch
     t0 = time.perf_counter()
     cfg = cfg or TreeConfig()
-    if not points.evals_alias_sources:
-        raise ValueError("the distributed engine evaluates at the sources (aliased evaluation "
-                         "points); use fmm_evaluate for separate evaluation points")
     comm = Comm(group)
     dev_index = torch.cuda.current_device() if device is None else int(device)
     dev = torch.device("cuda", dev_index)
     ctx = _lib.default_context(dev_index)
-    n = points.n_sources
+    n, m = points.n_sources, points.n_evals
     lo, hi = shard_bounds(n, comm.size, comm.rank)
+    separate = not points.evals_alias_sources
     with ctx.lock, torch.cuda.device(dev), torch.cuda.stream(engine_stream(dev_index)):
+        pos = torch.from_numpy(np.ascontiguousarray(points.positions[lo:hi])
+                               .view(np.float64).reshape(-1, 2)).to(dev)
+        gam = torch.from_numpy(np.ascontiguousarray(points.strengths[lo:hi])).to(dev)
+
+        def run(as_separate):
+            evals = None
+            if as_separate:
+                elo, ehi = shard_bounds(m, comm.size, comm.rank)
+                src = points.eval_positions if separate else points.positions
+                epos = torch.from_numpy(np.ascontiguousarray(src[elo:ehi])
+                                        .view(np.float64).reshape(-1, 2)).to(dev)
+                evals = (m, epos, elo)
+            return evaluate_shard(ctx, comm, n, pos, gam, lo, cfg, evals)
+
+        # the library stays on the engine stream (dist_end) until the gather's
+        # scatter kernel and the report queries are done
         try:
-            pos = torch.from_numpy(np.ascontiguousarray(points.positions[lo:hi])
-                                   .view(np.float64).reshape(-1, 2)).to(dev)
-            gam = torch.from_numpy(np.ascontiguousarray(points.strengths[lo:hi])).to(dev)
-            vals, idx, rep = evaluate_shard(ctx, comm, n, pos, gam, lo, cfg)
-            if gather:
-                n_max = torch.tensor([vals.shape[0]], dtype=torch.int64)
-                if not comm.staged:
-                    n_max = n_max.to(dev)
-                comm.allreduce(n_max, "max")
-                nm = int(n_max.item())
-                pv = torch.zeros((nm, 2), dtype=torch.float64, device=dev)
-                pi = torch.full((nm,), -1, dtype=torch.int64, device=dev)
-                pv[:vals.shape[0]] = vals
-                pi[:idx.shape[0]] = idx
-                av = torch.empty((comm.size * nm, 2), dtype=torch.float64, device=dev)
-                ai = torch.empty(comm.size * nm, dtype=torch.int64, device=dev)
-                comm.all_gather(av, pv)
-                comm.all_gather(ai, pi)
-                keep = ai >= 0
-                av, ai = av[keep].contiguous(), ai[keep].contiguous()
-                out = torch.empty((n, 2), dtype=torch.float64, device=dev)
-                ctx.check(ctx.lib.fmm2d_scatter_values(ctx.h, ai.shape[0],
-                                                       C.c_void_p(av.data_ptr()),
-                                                       C.c_void_p(ai.data_ptr()),
-                                                       C.c_void_p(out.data_ptr())))
-                values = out.cpu().numpy().view(np.complex128).reshape(-1)
-            else:
-                values = (vals.cpu().numpy().view(np.complex128).reshape(-1), idx.cpu().numpy())
-            torch.cuda.current_stream(dev).synchronize()
-            wall = time.perf_counter() - t0
-            report = _merge_report(ctx, comm, rep, wall, n)
+            try:
+                vals, idx, rep = run(separate)
+            except ValueError as e:
+                if separate or "ties" not in str(e):
+                    raise
+                vals, idx, rep = run(True)
+            return _gather_and_report(ctx, comm, dev, vals, idx, rep, gather, m,
+                                      0 if separate else n, t0)
         finally:
             ctx.lib.fmm2d_dist_end(ctx.h)
+
+
+def _gather_and_report(ctx, comm, dev, vals, idx, rep, gather, m, self_skips, t0):
+    """Values of all evaluation points in input order (gather) or this rank's
+    owned ones, plus the merged report; runs on the engine stream."""
+    import torch
+    if gather:
+        n_max = torch.tensor([vals.shape[0]], dtype=torch.int64)
+        if not comm.staged:
+            n_max = n_max.to(dev)
+        comm.allreduce(n_max, "max")
+        nm = int(n_max.item())
+        pv = torch.zeros((nm, 2), dtype=torch.float64, device=dev)
+        pi = torch.full((nm,), -1, dtype=torch.int64, device=dev)
+        pv[:vals.shape[0]] = vals
+        pi[:idx.shape[0]] = idx
+        av = torch.empty((comm.size * nm, 2), dtype=torch.float64, device=dev)
+        ai = torch.empty(comm.size * nm, dtype=torch.int64, device=dev)
+        comm.all_gather(av, pv)
+        comm.all_gather(ai, pi)
+        keep = ai >= 0
+        av, ai = av[keep].contiguous(), ai[keep].contiguous()
+        out = torch.empty((m, 2), dtype=torch.float64, device=dev)
+        ctx.check(ctx.lib.fmm2d_scatter_values(ctx.h, ai.shape[0], C.c_void_p(av.data_ptr()),
+                                               C.c_void_p(ai.data_ptr()),
+                                               C.c_void_p(out.data_ptr())))
+        values = out.cpu().numpy().view(np.complex128).reshape(-1)
+    else:
+        values = (vals.cpu().numpy().view(np.complex128).reshape(-1), idx.cpu().numpy())
+    torch.cuda.current_stream(dev).synchronize()
+    wall = time.perf_counter() - t0
+    # coincident_skips excludes the points' meetings with themselves only
+    # when the evaluation points alias the sources (engine.py:271-275)
+    report = _merge_report(ctx, comm, rep, wall, self_skips)
     report.total_seconds = time.perf_counter() - t0
     return values, report

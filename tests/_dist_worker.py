@@ -47,12 +47,23 @@ def comm_checks(out):
         Path(out).write_text(json.dumps(parts))
 
 
+def engine_inputs(kind, n, m=None):
+    """Sources (seed 7); with m, m separate evaluation points (uniform, seed 8)."""
+    import paper_1205_4611_b200 as F
+    pts = F.sample_points(F.DistributionSpec(kind, 0.01, 7), int(n))
+    if m:
+        ev = F.sample_points(F.DistributionSpec("uniform", 0.01, 8), int(m)).positions
+        pts = F.ParticleSet(pts.positions, pts.strengths, ev)
+    return pts
+
+
 def engine_run(spec, out):
     import torch
     import paper_1205_4611_b200 as F
     from paper_1205_4611_b200.distributed import fmm_evaluate_distributed
-    _, kind, n, p = spec.split(":")
-    pts = F.sample_points(F.DistributionSpec(kind, 0.01, 7), int(n))
+    parts = spec.split(":")
+    kind, n, p = parts[1], parts[2], parts[3]
+    pts = engine_inputs(kind, n, parts[4] if len(parts) > 4 else None)
     cfg = F.TreeConfig(35, 0.5, int(p))
     vals, rep = fmm_evaluate_distributed(pts, cfg, device=0)
     (own, idx), _ = fmm_evaluate_distributed(pts, cfg, device=0, gather=False)
@@ -81,17 +92,21 @@ def failure_inputs(case):
 
 
 def raise_run(case, out):
-    """Every rank must leave the evaluation with the same exception (none
-    may hang in a collective); rank 0 records all outcomes."""
+    """Every rank must leave the evaluation with the same outcome (none may
+    hang in a collective); rank 0 records all outcomes (and, on success, the
+    gathered values)."""
     import torch.distributed as dist
     import paper_1205_4611_b200 as F
     from paper_1205_4611_b200.distributed import fmm_evaluate_distributed
     pts = failure_inputs(case)
+    vals = None
     try:
-        fmm_evaluate_distributed(pts, F.TreeConfig(35, 0.5, 12), device=0)
+        vals, _ = fmm_evaluate_distributed(pts, F.TreeConfig(35, 0.5, 12), device=0)
         res = None
     except Exception as e:     # noqa: BLE001 -- recorded for the test
         res = [type(e).__name__, str(e)]
+    if vals is not None and int(os.environ["RANK"]) == 0:
+        np.save(str(out) + ".npy", vals)
     parts = [None] * dist.get_world_size()
     dist.all_gather_object(parts, res)
     if int(os.environ["RANK"]) == 0:

@@ -91,25 +91,81 @@ def test_distributed_nccl_single_rank(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world,exc", [("degenerate", 2, "DegenerateInputError"),
-                                            ("degenerate", 4, "DegenerateInputError"),
-                                            ("ties", 2, "ValueError")])
-def test_distributed_failures_raise_on_every_rank(tmp_path, case, world, exc):
-    """A failure detected by one rank only (a degenerate box inside its
-    subtree) or by the collective top split (ties at a median cut) ends the
-    evaluation on EVERY rank with the same exception type -- no rank blocks in
-    a collective (dist.cu error agreement).  The single-GPU engine
-    raises the same type on the same inputs (ties: it re-splits instead)."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_degenerate_raises_on_every_rank(tmp_path, world):
+    """A degenerate box inside ONE rank's subtree ends the evaluation on EVERY
+    rank with DegenerateInputError (dist.cu error agreement) -- no
+    rank blocks in a collective -- as the single-GPU engine does."""
     sys.path.insert(0, str(ROOT / "tests"))
     import _dist_worker as W
     import paper_1205_4611_b200 as F
     out = tmp_path / "raise.json"
-    launch(world, f"raise:{case}", out, 29700 + world + len(case), timeout=300)
+    launch(world, "raise:degenerate", out, 29700 + world, timeout=300)
     parts = json.loads(out.read_text())
-    assert all(p is not None and p[0] == exc for p in parts), parts
+    assert all(p is not None and p[0] == "DegenerateInputError" for p in parts), parts
     assert len({p[1] for p in parts}) == 1, parts
-    if case == "degenerate":
-        with pytest.raises(F.DegenerateInputError):
-            F.fmm_evaluate(W.failure_inputs(case), F.TreeConfig(35, 0.5, 12), device=0)
-    else:
-        assert "ties" in parts[0][1]
+    with pytest.raises(F.DegenerateInputError):
+        F.fmm_evaluate(W.failure_inputs("degenerate"), F.TreeConfig(35, 0.5, 12), device=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_ties_at_a_cut_match_single_gpu(tmp_path, world):
+    """A 39 x 40 lattice: the first median cut falls inside a column of equal
+    x, so the reference's evaluation split (coord <= cut) differs from the
+    source split.  Every rank agrees on the tie and reruns with the points as
+    separate evaluation points (dist.cu:198); values equal the
+    single-GPU engine's (which re-splits the same way) to roundoff."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _dist_worker as W
+    import paper_1205_4611_b200 as F
+    out = tmp_path / "ties.json"
+    launch(world, "raise:ties", out, 29710 + world, timeout=300)
+    parts = json.loads(out.read_text())
+    assert all(p is None for p in parts), parts
+    vals = np.load(str(out) + ".npy")
+    pts = W.failure_inputs("ties")
+    ref, _ = F.fmm_evaluate(pts, F.TreeConfig(35, 0.5, 12), device=0)
+    assert np.max(np.abs(vals - ref) / np.abs(ref)) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,kind,n,m,p", [(2, "uniform", 20000, 15000, 20),
+                                              (4, "normal", 30000, 24000, 30),
+                                              (8, "uniform", 40000, 9000, 17)])
+def test_distributed_separate_evaluation_points(tmp_path, world, kind, n, m, p):
+    """Separate evaluation points (the C4 shape) across ranks: routed to the
+    rank owning their top-split segment by coord <= cut, evaluated there, values
+    gathered in input order -- equal to the single-GPU engine to roundoff, with
+    the same list totals and coincident-skip count."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _dist_worker as W
+    import paper_1205_4611_b200 as F
+    out = tmp_path / "sep.npz"
+    launch(world, f"engine:{kind}:{n}:{p}:{m}", out, 29720 + world + n % 89)
+    d = np.load(out)
+    pts = W.engine_inputs(kind, n, m)
+    ref, rep = F.fmm_evaluate(pts, F.TreeConfig(35, 0.5, p), device=0)
+    vals = d["values"]
+    assert vals.shape == (m,)
+    assert np.max(np.abs(vals - ref) / np.abs(ref)) <= 1e-13
+    np.testing.assert_array_equal(vals[d["idx"]], d["own"])
+    drep = json.loads(str(d["report"]))
+    assert drep["totals"] == rep.list_totals
+    assert drep["skips"] == rep.coincident_skips
+
+
+@pytest.mark.gpu
+def test_distributed_matches_oracle(tmp_path):
+    """4 ranks against the CPU oracle directly (not only against the GPU
+    engine): potentials <= 1e-12 relative on normal inputs."""
+    sys.path.insert(0, str(ROOT))
+    from oracle import fmm2d_oracle as O
+    out = tmp_path / "orc.npz"
+    launch(4, "engine:normal:30000:20", out, 29740)
+    d = np.load(out)
+    sys.path.insert(0, str(ROOT / "tests"))
+    import _dist_worker as W
+    pts = W.engine_inputs("normal", 30000)
+    ref, _, _, _ = O.fmm(pts.positions, pts.strengths, None, 35, 0.5, 20)
+    assert O.max_rel(d["values"], ref) <= 1e-12
