@@ -338,24 +338,36 @@ def run_dist(args, cfg, ws, rank, local):
     else:
         dist.init_process_group(backend)
     comm = Comm()
-    if cfg["m"] is not None:
-        raise SystemExit("multi-GPU bench runs the aliased configurations (c2, c3, c5)")
     tcfg = F.TreeConfig(35, 0.5, cfg["p"])
     n_total = ws * cfg["n"]
     pts = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 0), n_total)
+    m_total = n_total
+    if cfg["m"] is not None:      # C4: separate evaluation points, weak-scaled too
+        m_total = ws * cfg["m"]
+        ev = F.sample_points(F.DistributionSpec(cfg["kind"], 0.01, 1), m_total).positions
+        pts = F.ParticleSet(pts.positions, pts.strengths, ev)
     lo, hi = shard_bounds(n_total, ws, rank)
     st = engine_stream(local)
     ctx = _lib.default_context(local)
+    evals = None
     with torch.cuda.stream(st):
         d_pos = torch.from_numpy(pts.positions[lo:hi].view(np.float64).reshape(-1, 2)).to(dev)
         d_g = torch.from_numpy(pts.strengths[lo:hi].copy()).to(dev)
+        if cfg["m"] is not None:
+            elo, ehi = shard_bounds(m_total, ws, rank)
+            d_epos = torch.from_numpy(np.ascontiguousarray(pts.eval_positions[elo:ehi])
+                                      .view(np.float64).reshape(-1, 2)).to(dev)
+            evals = (m_total, d_epos, elo)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step():
         with torch.cuda.stream(st):
             e0.record(st)
-            vals, idx, rep = evaluate_shard(ctx, comm, n_total, d_pos, d_g, lo, tcfg)
+            try:
+                vals, idx, rep = evaluate_shard(ctx, comm, n_total, d_pos, d_g, lo, tcfg, evals)
+            finally:
+                ctx.lib.fmm2d_dist_end(ctx.h)
             e1.record(st)
         st.synchronize()
         return e0.elapsed_time(e1), rep
@@ -415,7 +427,8 @@ def run_dist(args, cfg, ws, rank, local):
                    "l2": "flushed between timed steps (512 MiB write)"},
         "phase_ms": {k: round(v, 4) for k, v in zip(names, phase)},
         "e2e": {"value": n_total / e2e_s, "unit": "particles/s",
-                "h2d_bytes_per_step": 24 * (hi - lo), "d2h_bytes_per_step": 24 * len(own),
+                "h2d_bytes_per_step": 24 * (hi - lo) + (16 * int(evals[1].shape[0]) if evals else 0),
+                "d2h_bytes_per_step": 24 * len(own),
                 "ms_per_step": e2e_s * 1e3},
         "roofline": {"kernel": "m2l", "bound": "fp64", "pipe": "fp64 (DMMA = DFMA peak)",
                      "achieved": achieved, "peak": peak,
