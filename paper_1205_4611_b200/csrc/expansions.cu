@@ -25,7 +25,8 @@ namespace fmm {
 namespace {
 
 constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:37-38
-constexpr int M2P_INLINE = 16;   // m2p sources per point handled by k_l2p_m2p itself
+constexpr int M2P_INLINE = 16;
+   // m2p sources per point handled by k_l2p_m2p itself
 // M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
 // target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
 bool m2l_force_target() {
@@ -73,8 +74,10 @@ __device__ __forceinline__ double dxor(double a, unsigned long long s) {
   return __longlong_as_double(__double_as_longlong(a) ^ s);
 }
 
+// coefficient j of a row of p + 1, zero above p; EX: p == PM is known, no test
+template <bool EX = false>
 __device__ __forceinline__ cplx ld_coef(const double2* base, int j, int p) {
-  if (j > p) return cplx{0.0, 0.0};
+  if (!EX && j > p) return cplx{0.0, 0.0};
   double2 v = base[j];
   return cplx{v.x, v.y};
 }
@@ -815,7 +818,7 @@ __global__ void k_m2l_fixup(const int* __restrict__ lo_ptr, const int* __restric
 // in y - z0), then += each m2p source in ascending order (operators.py:
 // 358-386).  Coefficient rows stream from L1/L2 (the points of one leaf
 // share them), all loads of a row in flight at once.
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(128)
 k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __restrict__ eleaf,
           const double2* __restrict__ eval_pos, const int* __restrict__ m_off,
@@ -833,7 +836,7 @@ k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __rest
   const double2* bl = local + (lb + b) * (p + 1);
   cplx c[PM + 1];
 #pragma unroll
-  for (int j = 0; j <= PM; ++j) c[j] = ld_coef(bl, j, p);
+  for (int j = 0; j <= PM; ++j) c[j] = ld_coef<EX>(bl, j, p);
   cplx acc = c[PM];
 #pragma unroll
   for (int j = PM - 1; j >= 0; --j) acc = cadd(cmul(acc, w), c[j]);
@@ -849,7 +852,7 @@ k_l2p_m2p(long long m, long long e0, long long e1, int L, const unsigned* __rest
     const cplx inv = crcp_fast(u);
     const double2* a = mult + ga * (p + 1);
 #pragma unroll
-    for (int j = 1; j <= PM; ++j) c[j] = ld_coef(a, j, p);
+    for (int j = 1; j <= PM; ++j) c[j] = ld_coef<EX>(a, j, p);
     cplx h = c[PM];
 #pragma unroll
     for (int j = PM - 1; j >= 1; --j) h = cadd(cmul(h, inv), c[j]);
@@ -873,7 +876,7 @@ __global__ void k_m2p_find_long(long long b0, long long b1, const int* __restric
   if (b < b1 && m_off[b + 1] - m_off[b] > M2P_INLINE) list[atomicAdd(count, 1)] = (int)b;
 }
 
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(M2P_LONG_THREADS)
 k_m2p_long(int L, const int* __restrict__ list, const int* __restrict__ count,
            const int* __restrict__ eoff, const double2* __restrict__ eval_pos,
@@ -904,7 +907,7 @@ k_m2p_long(int L, const int* __restrict__ list, const int* __restrict__ count,
         const double2* a = mult + ga * (p + 1);
         cplx c[PM + 1];
 #pragma unroll
-        for (int j = 1; j <= PM; ++j) c[j] = ld_coef(a, j, p);
+        for (int j = 1; j <= PM; ++j) c[j] = ld_coef<EX>(a, j, p);
         const double ax = cx[ga], ay = cy[ga];
 #pragma unroll
         for (int k = 0; k < M2P_LONG_POINTS; ++k) {
@@ -1099,7 +1102,9 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
   if (e1 <= e0) return;
   dispatch_p(E.p, [&](auto pm) {
     note_launch();
-    launch(k_l2p_m2p<decltype(pm)::value>, nblk(e1 - e0, 128), 128, 0, st, 
+    constexpr int PMv = decltype(pm)::value;
+    const bool ex = E.p == PMv;         // exact order: no per-coefficient range tests
+    launch(ex ? k_l2p_m2p<PMv, true> : k_l2p_m2p<PMv, false>, nblk(e1 - e0, 128), 128, 0, st,
         T.m, e0, e1, T.L, T.eleaf_t, T.epos_t, Ls.m2p_off.as<int>(), Ls.m2p_idx.as<int>(),
         T.box_cx.as<double>(), T.box_cy.as<double>(), E.mult.as<double2>(),
         E.local.as<double2>(), E.phi.as<double2>(), E.p, dstat);
@@ -1117,7 +1122,7 @@ void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus
     launch(k_m2p_find_long, nblk(b1 - b0, 256), 256, 0, st, b0, b1, Ls.m2p_off.as<int>(),
                                                         E.long_list.as<int>(), cnt);
     note_launch();
-    launch(k_m2p_long<decltype(pm)::value>, 2 * 148, M2P_LONG_THREADS, 0, st, 
+    launch(ex ? k_m2p_long<PMv, true> : k_m2p_long<PMv, false>, 2 * 148, M2P_LONG_THREADS, 0, st,
         T.L, E.long_list.as<int>(), cnt, T.eoff_t, T.epos_t, Ls.m2p_off.as<int>(),
         Ls.m2p_idx.as<int>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.mult.as<double2>(), E.phi.as<double2>(), E.p, dstat);
