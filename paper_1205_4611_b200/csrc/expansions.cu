@@ -84,12 +84,13 @@ __device__ __forceinline__ cplx ld_coef(const double2* base, int j, int p) {
 
 // --------------------------------------------------------------------------
 // P2M (engine.py:67-82): one thread per leaf, sequential over its sources
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(128)
 k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
       const double2* __restrict__ src_pos, const double* __restrict__ src_g,
       const double* __restrict__ cx, const double* __restrict__ cy, double2* mult, int p) {
   pdl_enter();
+  if constexpr (EX) p = PM;                       // exact order: compile-time p
   const long long b = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (b >= b1) return;
   const long long gb = level_base(L) + b;
@@ -121,7 +122,7 @@ k_p2m(int L, long long b0, long long b1, const int* __restrict__ offL,
 //  k_p2l_fold: one thread per target leaf adds its pairs' rows in ascending
 //    source order (the reference's local[b] += ... sequence) and initialises
 //    local[L] (zero without p2l sources).
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(128)
 k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
            const int* __restrict__ l_off, const int* __restrict__ l_idx,
@@ -129,6 +130,7 @@ k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
            const double* __restrict__ cx, const double* __restrict__ cy, double2* rows, int p,
            DevStatus* st) {
   pdl_enter();
+  if constexpr (EX) p = PM;                       // exact order: compile-time p
   if (lists_overflowed(st)) return;
   const long long lb = level_base(L);
   const int qbase = l_off[b0], qend = l_off[b1];
@@ -218,11 +220,12 @@ __device__ __forceinline__ void m2m_shift(cplx (&a)[PM + 1], cplx r) {
 
 // four threads per parent (one per child shift), children summed in order
 // 0..3 through shuffles (engine.py:100 reshape(-1, 4, p+1).sum(1))
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(128)
 k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* mult, int p) {
   pdl_enter();
+  if constexpr (EX) p = PM;                       // exact order: compile-time p
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long k = k0 + (t >> 2);
   const int c = (int)(t & 3), lane = threadIdx.x & 31;
@@ -249,11 +252,12 @@ k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
 
 // --------------------------------------------------------------------------
 // L2L (engine.py:126-129, operators.py:151-186): thread per child
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(128)
 k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
       const double* __restrict__ cy, double2* local, int p) {
   pdl_enter();
+  if constexpr (EX) p = PM;                       // exact order: compile-time p
   // parent level l, child level l+1 (children [c0, c1))
   const long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (c >= c1) return;
@@ -400,7 +404,7 @@ __device__ __forceinline__ void m2l_load_pair(M2LPair<PM>& P, long long i, long 
   for (int k = 1; k <= PM; ++k) P.a[k - 1] = k <= p ? a[k] : make_double2(0.0, 0.0);
 }
 
-template <int PM>
+template <int PM, bool EX>
 __global__ void __launch_bounds__(M2L_ITEM, M2LDenseCfg<PM>::MINB)
 k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
             const int* __restrict__ w_src, const int* __restrict__ w_tgt,
@@ -409,6 +413,7 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
             unsigned char* item_flags, int p, DevStatus* st) {
   pdl_enter();
   static_assert(PM <= 32, "dense M2L is compiled for PM <= 32");
+  if constexpr (EX) p = PM;                       // exact order: p is a compile-time constant
   using Cfg = M2LDenseCfg<PM>;
   if (lists_overflowed(st)) return;
   extern __shared__ double red[];                 // [R][STR]
@@ -958,14 +963,15 @@ struct Launch {
     const long long b0 = part.lo(L), b1 = part.hi(L);
     if (which != 2) {
       note_launch();
-      launch(k_p2m<PM>, nblk(b1 - b0, 128), 128, 0, st, L, b0, b1, offL, T.src_pos.as<double2>(),
+      launch(p == PM ? k_p2m<PM, true> : k_p2m<PM, false>, nblk(b1 - b0, 128), 128, 0, st, L, b0,
+             b1, offL, T.src_pos.as<double2>(),
              T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
              E.mult.as<double2>(), p);
     }
     if (which == 1) return;
     note_launch();
     E.p2l_rows.reserve(sizeof(double2) * std::max(1ll, Ls.cap_p2l) * (p + 1));
-    launch(k_p2l_pair<PM>, 8 * sm_count(), 128, 0, st, 
+    launch(p == PM ? k_p2l_pair<PM, true> : k_p2l_pair<PM, false>, 8 * sm_count(), 128, 0, st,
         L, b0, b1, offL, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), T.src_pos.as<double2>(),
         T.src_g.as<double>(), T.box_cx.as<double>(), T.box_cy.as<double>(),
         E.p2l_rows.as<double2>(), p, dstat);
@@ -979,7 +985,8 @@ struct Launch {
     for (int l = lmax; l >= lmin; --l) {
       const long long k0 = part.lo(l), k1 = part.hi(l);
       note_launch();
-      launch(k_m2m<PM>, nblk(4 * (k1 - k0), 128), 128, 0, st, l, k0, k1, T.box_cx.as<double>(),
+      launch(E.p == PM ? k_m2m<PM, true> : k_m2m<PM, false>, nblk(4 * (k1 - k0), 128), 128, 0, st,
+             l, k0, k1, T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), E.mult.as<double2>(),
                                                     E.p);
     }
@@ -1014,12 +1021,14 @@ struct Launch {
             T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
             E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
       } else {
-        static unsigned attr_dense = 0;
-        ensure_smem_attr(k_m2l_dense<PM>, Cfg::SMEM, attr_dense);
+        static unsigned attr_dense[2] = {0, 0};
+        const bool ex = E.p == PM;
+        auto kern = ex ? k_m2l_dense<PM, true> : k_m2l_dense<PM, false>;
+        ensure_smem_attr(kern, Cfg::SMEM, attr_dense[ex]);
         const unsigned grid = (unsigned)std::min<long long>(
             std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
         note_launch();
-        launch(k_m2l_dense<PM>, grid, M2L_ITEM, Cfg::SMEM, st,
+        launch(kern, grid, M2L_ITEM, Cfg::SMEM, st,
             lo, total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
             T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
             E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
@@ -1044,7 +1053,8 @@ struct Launch {
     for (int l = 1; l < T.L; ++l) {
       const long long c0 = part.lo(l + 1), c1 = part.hi(l + 1);
       note_launch();
-      launch(k_l2l<PM>, nblk(c1 - c0, 128), 128, 0, st, l, c0, c1, T.box_cx.as<double>(),
+      launch(E.p == PM ? k_l2l<PM, true> : k_l2l<PM, false>, nblk(c1 - c0, 128), 128, 0, st, l,
+             c0, c1, T.box_cx.as<double>(),
                                                     T.box_cy.as<double>(), E.local.as<double2>(),
                                                     E.p);
     }
