@@ -413,6 +413,7 @@ class OResult:
     mult: list = field(default_factory=list)
     local: list = field(default_factory=list)
     phi_sorted: np.ndarray | None = None
+    phi_far: np.ndarray | None = None     # tree order, L2P + M2P only (before P2P)
 
 
 def p2m_leaves(T: OTree, p):
@@ -488,6 +489,7 @@ def evaluate(T: OTree, Ls: OLists, p: int, timings=True) -> OResult:
             for a in Ls.m2p_idx[Ls.m2p_off[b]:Ls.m2p_off[b + 1]]:
                 phi[e0:e1] += op_m2p(mult[L][a], T.center[L][a], T.eval_pos[e0:e1])
     t["l2p"] = time.perf_counter() - t0
+    phi_far = phi.copy()
 
     t0 = time.perf_counter()
     skips = 0
@@ -506,7 +508,7 @@ def evaluate(T: OTree, Ls: OLists, p: int, timings=True) -> OResult:
     values = np.empty_like(phi)
     values[T.eval_perm] = phi                        # engine.py:266-267
     expected_self = T.eval_pos.size if T.aliased else 0
-    return OResult(values, skips, max(0, skips - expected_self), t, mult, local, phi)
+    return OResult(values, skips, max(0, skips - expected_self), t, mult, local, phi, phi_far)
 
 
 def fmm(positions, strengths, eval_positions=None, nd=35, theta=0.5, p=17):

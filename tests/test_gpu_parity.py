@@ -126,10 +126,11 @@ def test_engine_matches_oracle(kind, n, seed, m, cluster, cfg):
     assert report.n_levels == T.n_levels
 
 
-def test_phase_expansions_match_oracle():
-    """Per-phase seam: multipole and local coefficients of every box
+def test_phase_seams_match_oracle():
+    """Per-phase seams: multipole and local coefficients of every box
     (P2M+M2M and P2L+M2L+L2L) against the oracle, relative to each box's
-    coefficient norm."""
+    coefficient norm, and the far field at every evaluation point (L2P + M2P,
+    before P2P; engine.py:132-160) against the oracle's."""
     pts = F.sample_points(F.DistributionSpec("uniform", seed=21), 20_000)
     cfg = F.TreeConfig(35, 0.5, 20)
     T = O.build_tree(pts.positions, pts.strengths, None, cfg.n_desired_per_box)
@@ -143,7 +144,11 @@ def test_phase_expansions_match_oracle():
             scale[scale == 0] = 1.0
             assert np.max(np.abs(got - want) / scale) <= 1e-12, lev
     phi = F.engine.export_phi(pts.n_evals)
-    assert np.all(np.isfinite(phi))
+    want = R.phi_far
+    assert phi.shape == want.shape
+    assert np.max(np.abs(phi - want)) <= 1e-12 * np.max(np.abs(want))
+    rel = np.abs(phi - want) / np.abs(want)
+    assert np.median(rel) <= 1e-14, float(np.median(rel))
 
 
 def test_tie_runs_of_rank_keys_fall_back_to_exact_keys():
