@@ -391,6 +391,17 @@ struct M2LPair {
   double2 a[PM];
 };
 
+// the pair's source row, its (target, source) indices already in hand
+template <int PM>
+__device__ __forceinline__ void m2l_load_row(M2LPair<PM>& P, int t, int s,
+                                             const double2* __restrict__ mult, int p) {
+  P.t = t;
+  P.s = s;
+  const double2* a = mult + (long long)s * (p + 1);
+#pragma unroll
+  for (int k = 1; k <= PM; ++k) P.a[k - 1] = k <= p ? a[k] : make_double2(0.0, 0.0);
+}
+
 template <int PM>
 __device__ __forceinline__ void m2l_load_pair(M2LPair<PM>& P, long long i, long long npairs,
                                               const int* __restrict__ w_src,
@@ -430,9 +441,23 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
   const long long ibase = lo ? lo / M2L_ITEM + 1 : 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   M2LPair<PM> P;
+  // (target, source) of this thread's pair in the first item; every item
+  // prefetches the next item's pair indices, so an item start waits on one
+  // round trip (the source row) instead of two
+  int nt_t = -1, nt_s = 0;
+  if (blockIdx.x < nitems) {
+    const long long i = lo + (long long)blockIdx.x * M2L_ITEM + tid;
+    nt_t = i < hi ? __ldg(w_tgt + i) : -1;
+    nt_s = i < hi ? __ldg(w_src + i) : 0;
+  }
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     const long long i0 = lo + it * M2L_ITEM, item = ibase + it;
-    m2l_load_pair<PM>(P, i0 + tid, hi, w_src, w_tgt, mult, p);
+    m2l_load_row<PM>(P, nt_t, nt_s, mult, p);
+    {
+      const long long inext = i0 + (long long)gridDim.x * M2L_ITEM + tid;
+      nt_t = inext < hi ? __ldg(w_tgt + inext) : -1;
+      nt_s = inext < hi ? __ldg(w_src + inext) : 0;
+    }
     // targets just before / after the item (segments continuing across items)
     const int prev_t = it > 0 ? __ldg(w_tgt + i0 - 1) : -1;
     const long long nxt = i0 + M2L_ITEM;
@@ -514,6 +539,11 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
       const int sg = task / R, r = task - sg * R;
       const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
       const double* row = red + r * Cfg::STR;
+      // an in-place target's old value is fetched before the sum (its global
+      // round trip overlaps the SMEM reads)
+      const bool sb = sg == 0 && first_cont, ea = sg == nseg - 1 && last_cont;
+      double* dst = reinterpret_cast<double*>(local + (long long)s_t[q0] * (p + 1)) + r;
+      const double old = (!sb && !ea) ? *dst : 0.0;
       // four interleaved chains (fixed order), then ((0+1)+(2+3))
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int q = q0;
@@ -526,8 +556,11 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
       if (q < q1) a0 += row[q];
       if (q + 1 < q1) a1 += row[q + 1];
       if (q + 2 < q1) a2 += row[q + 2];
-      m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, (a0 + a1) + (a2 + a3),
-               sg == 0 && first_cont, sg == nseg - 1 && last_cont, false);
+      const double v = (a0 + a1) + (a2 + a3);
+      if (!sb && !ea)
+        *dst = old + v;
+      else
+        m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, v, sb, ea, false);
     }
     // the item's chain flags as one byte store (no memset, no atomics): 1 head
     // part in slot 0, 2 tail part in slot 1, 5 the whole item continues a chain
