@@ -24,7 +24,11 @@ namespace {
 
 constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
-constexpr int P2P_CHUNK = 256;      // near sources staged per warp per round
+// near sources staged per warp per round: 256 for leaves of <= 32 points
+// (C2: ~210 near sources per leaf, one round), 512 for the two-block kernel
+// (C5: ~510 per leaf -- one round instead of two; 48 KB of SMEM per CTA;
+// measured C5 P2P 4.12 -> 3.88 ms, C2 unchanged with 256)
+constexpr int P2P_CHUNK1 = 256, P2P_CHUNK2 = 512;
 #ifndef P2P_SCAN
 #define P2P_SCAN 1
 #endif
@@ -195,6 +199,7 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
       const double2* __restrict__ eval_pos, const int* __restrict__ eval_perm,
       const double2* __restrict__ phi_in, double2* values, long long out_base, DevStatus* st) {
   pdl_enter();
+  constexpr int P2P_CHUNK = DUAL ? P2P_CHUNK2 : P2P_CHUNK1;
   __shared__ double2 s_pos[P2P_WARPS][P2P_CHUNK];
   __shared__ double s_g[P2P_WARPS][P2P_CHUNK];
   const long long b = b0 + ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
