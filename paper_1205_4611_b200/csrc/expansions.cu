@@ -409,7 +409,7 @@ __device__ __forceinline__ void m2l_load_pair(M2LPair<PM>& P, long long i, long 
                                               const double2* __restrict__ mult, int p) {
   const bool valid = i < npairs;
   P.t = valid ? __ldg(w_tgt + i) : -1;
-  P.s = valid ? __ldg(w_src + i) : 0;
+  P.s = valid ? __ldg(w_src + i) : 1;   // padding lanes read box 1's (computed) row
   const double2* a = mult + (long long)P.s * (p + 1);
 #pragma unroll
   for (int k = 1; k <= PM; ++k) P.a[k - 1] = k <= p ? a[k] : make_double2(0.0, 0.0);
@@ -448,7 +448,7 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
   if (blockIdx.x < nitems) {
     const long long i = lo + (long long)blockIdx.x * M2L_ITEM + tid;
     nt_t = i < hi ? __ldg(w_tgt + i) : -1;
-    nt_s = i < hi ? __ldg(w_src + i) : 0;
+    nt_s = i < hi ? __ldg(w_src + i) : 1;
   }
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     const long long i0 = lo + it * M2L_ITEM, item = ibase + it;
@@ -456,7 +456,7 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
     {
       const long long inext = i0 + (long long)gridDim.x * M2L_ITEM + tid;
       nt_t = inext < hi ? __ldg(w_tgt + inext) : -1;
-      nt_s = inext < hi ? __ldg(w_src + inext) : 0;
+      nt_s = inext < hi ? __ldg(w_src + inext) : 1;
     }
     // targets just before / after the item (segments continuing across items)
     const int prev_t = it > 0 ? __ldg(w_tgt + i0 - 1) : -1;
@@ -643,7 +643,7 @@ k_m2l_dmma(const int* __restrict__ total_ptr, const int* __restrict__ w_src,
       const long long i = item * M2L_ITEM + slot;
       const bool valid = i < npairs;
       const int t = valid ? __ldg(w_tgt + i) : 0;
-      const int s = valid ? __ldg(w_src + i) : 0;
+      const int s = valid ? __ldg(w_src + i) : 1;
       const double rx = cx[s] - cx[t], ry = cy[s] - cy[t];        // source - target
       const bool sing = valid && rx == 0.0 && ry == 0.0;
       if (sing && tig == 0) atomicOr(&st->flags, ST_M2L_SINGULAR);
