@@ -7,6 +7,7 @@
 // are sized from capacities the context remembers; if a fill overflowed, the
 // status says so and the call regrows and reruns (the context keeps the
 // high-water mark, so steady-state calls never rerun).
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -196,6 +197,16 @@ bool capture_cut(int action) {
   return true;
 }
 
+// NVTX ranges around the host-side enqueue of each phase (header-only NVTX 3:
+// no cost unless a profiler is attached); the device-side phase times are the
+// CUDA events of the report
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // everything from the status reset to the status download, on c->st
 void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values, double* out,
                       bool device_io) {
@@ -207,7 +218,10 @@ void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values
   g_launches = 0;
   reset_status(c);
   rec_time(c->ev[0], c->st);
-  build_tree_impl(c, nd);
+  {
+    NvtxRange r("fmm2d.sort");
+    build_tree_impl(c, nd);
+  }
   rec_time(c->ev[1], c->st);
   const int* offL = c->plan.d_off.as<int>() + off_base(2 * L);
   // P2M and M2M need only the tree: they run on the side stream while the
@@ -227,7 +241,10 @@ void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values
   // (M2L of the coarse levels beside the finest level's connectivity, on the
   // side stream, was measured: the two compete for the SMs and the step time
   // stays within +-1 % at C2-C5, so M2L runs once after the lists)
-  run_connectivity(T, Ls, theta, dst, c->st);
+  {
+    NvtxRange r("fmm2d.connect");
+    run_connectivity(T, Ls, theta, dst, c->st);
+  }
   rec_time(c->ev[2], c->st);
   if (L > 0)
     FMM_CUDA(cudaMemsetAsync(E.local.p, 0, sizeof(double2) * level_base(L) * (p + 1), c->st));
@@ -236,14 +253,26 @@ void enqueue_pipeline(fmm2d_ctx* c, int p, double theta, int nd, double2* values
   if (overlap) FMM_CUDA(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   else run_m2m(T, E, c->st);
   rec_time(c->ev[4], c->st);
-  run_m2l(T, Ls, E, dst, c->st);
+  {
+    NvtxRange r("fmm2d.m2l");
+    run_m2l(T, Ls, E, dst, c->st);
+  }
   rec_time(c->ev[5], c->st);
-  run_l2l(T, E, dst, c->st);
+  {
+    NvtxRange r("fmm2d.l2l");
+    run_l2l(T, E, dst, c->st);
+  }
   rec_time(c->ev[6], c->st);
-  run_l2p_m2p(T, Ls, E, dst, c->st);
+  {
+    NvtxRange r("fmm2d.l2p_m2p");
+    run_l2p_m2p(T, Ls, E, dst, c->st);
+  }
   rec_time(c->ev[7], c->st);
   // P2P adds into phi and scatters to input order (engine.py:263-267)
-  run_p2p(T, Ls, E, offL, values, dst, c->st);
+  {
+    NvtxRange r("fmm2d.p2p");
+    run_p2p(T, Ls, E, offL, values, dst, c->st);
+  }
   rec_time(c->ev[8], c->st);
   // the result download starts now, on the copy stream beside the report
   // kernels, instead of after the status round trip (a retry simply rewrites
