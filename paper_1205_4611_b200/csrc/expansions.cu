@@ -147,19 +147,38 @@ k_p2l_pair(int L, long long b0, long long b1, const int* __restrict__ offL,
     cplx acc[PM + 1];
 #pragma unroll
     for (int j = 0; j <= PM; ++j) acc[j] = cplx{0.0, 0.0};
-    for (int i = offL[a]; i < offL[a + 1]; ++i) {
+    // two particles per step: their power chains are independent, and
+    // acc[k] = (acc[k] + w_i) + w_{i+1} keeps the sequential summation order
+    const int i0 = offL[a], i1 = offL[a + 1];
+    int i = i0;
+    for (; i + 2 <= i1; i += 2) {
+      const double2 z0 = src_pos[i], z1 = src_pos[i + 1];
+      const cplx d0{z0.x - x0, z0.y - y0}, d1{z1.x - x0, z1.y - y0};
+      const bool s0 = d0.x == 0.0 && d0.y == 0.0, s1 = d1.x == 0.0 && d1.y == 0.0;
+      if (s0 || s1) atomicOr(&st->flags, ST_P2L_SINGULAR);
+      const cplx inv0 = s0 ? cplx{0.0, 0.0} : crcp_fast(d0);
+      const cplx inv1 = s1 ? cplx{0.0, 0.0} : crcp_fast(d1);
+      cplx w0 = cscale(inv0, src_g[i]), w1 = cscale(inv1, src_g[i + 1]);
+#pragma unroll
+      for (int k = 0; k <= PM; ++k) {
+        acc[k] = cadd(cadd(acc[k], w0), w1);
+        w0 = cmul(w0, inv0);
+        w1 = cmul(w1, inv1);
+      }
+    }
+    if (i < i1) {
       const double2 z = src_pos[i];
       const cplx d{z.x - x0, z.y - y0};
       if (d.x == 0.0 && d.y == 0.0) {
         atomicOr(&st->flags, ST_P2L_SINGULAR);
-        continue;
-      }
-      const cplx inv = crcp_fast(d);
-      cplx w = cscale(inv, src_g[i]);
+      } else {
+        const cplx inv = crcp_fast(d);
+        cplx w = cscale(inv, src_g[i]);
 #pragma unroll
-      for (int k = 0; k <= PM; ++k) {
-        acc[k] = cadd(acc[k], w);
-        w = cmul(w, inv);
+        for (int k = 0; k <= PM; ++k) {
+          acc[k] = cadd(acc[k], w);
+          w = cmul(w, inv);
+        }
       }
     }
     double2* out = rows + (q - qbase) * (p + 1);
