@@ -183,6 +183,7 @@ struct ExpState {
   DBuf partials, item_flags;         // M2L cross-warp partial sums
   DBuf long_list;                    // leaves with long m2p lists (+ count)
   DBuf p2l_rows;                     // one P2L row per p2l pair
+  int l2l_chain_lt = 0;              // last L2L: levels 2..lt-1 left M2L-only (chained kernel)
 };
 
 // count of engine kernel launches (gpu_launches evidence in the report)
@@ -238,6 +239,9 @@ void run_m2l(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* ds
              cudaStream_t st);
 void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
              const Part& part = Part());
+// debug seam: `out` (a copy of E.local) gets the complete local expansions of
+// the levels the chained L2L kernel only passes through
+void complete_chained_locals(const TreeState& T, ExpState& E, double2* out, cudaStream_t st);
 // L2P + M2P for tree-ordered evaluation points [e0, e1) (e1 < 0: all)
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
                  cudaStream_t st, long long e0 = 0, long long e1 = -1,

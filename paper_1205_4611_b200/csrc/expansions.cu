@@ -26,6 +26,9 @@ namespace {
 
 constexpr double SCALED_LO = 1e-12, SCALED_HI = 1e12;   // operators.py:37-38
 constexpr int M2P_INLINE = 16;
+#ifndef L2L_CHAIN
+#define L2L_CHAIN 1      // chained kernel for the small top levels of the L2L pass
+#endif
    // m2p sources per point handled by k_l2p_m2p itself
 // M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
 // target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
@@ -271,22 +274,10 @@ k_m2m(int l, long long k0, long long k1, const double* __restrict__ cx,
 
 // --------------------------------------------------------------------------
 // L2L (engine.py:126-129, operators.py:151-186): thread per child
-template <int PM, bool EX>
-__global__ void __launch_bounds__(128)
-k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
-      const double* __restrict__ cy, double2* local, int p) {
-  pdl_enter();
-  if constexpr (EX) p = PM;                       // exact order: compile-time p
-  // parent level l, child level l+1 (children [c0, c1))
-  const long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (c >= c1) return;
-  const long long gc = level_base(l + 1) + c;
-  const long long gp = level_base(l) + (c >> 2);
-  const double2* src = local + gp * (p + 1);
-  cplx b[PM + 1];
-#pragma unroll
-  for (int j = 0; j <= PM; ++j) b[j] = ld_coef(src, j, p);
-  const cplx r{cx[gp] - cx[gc], cy[gp] - cy[gc]};                 // parent - child
+// the parent's incoming expansion b (in place) re-centred on the child:
+// r = parent - child (operators.py:151-186, scaled form inside the window)
+template <int PM>
+__device__ __forceinline__ void l2l_shift(cplx (&b)[PM + 1], cplx r) {
   const double mag = numpy_cabs(r.x, r.y);
   if (mag >= SCALED_LO && mag <= SCALED_HI) {
     cplx pw = r;
@@ -312,6 +303,24 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
 #pragma unroll
       for (int j = PM - k; j < PM; ++j) b[j] = csub(b[j], cmul(r, b[j + 1]));
   }
+}
+
+template <int PM, bool EX>
+__global__ void __launch_bounds__(128)
+k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
+      const double* __restrict__ cy, double2* local, int p) {
+  pdl_enter();
+  if constexpr (EX) p = PM;                       // exact order: compile-time p
+  // parent level l, child level l+1 (children [c0, c1))
+  const long long c = c0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  const long long gc = level_base(l + 1) + c;
+  const long long gp = level_base(l) + (c >> 2);
+  const double2* src = local + gp * (p + 1);
+  cplx b[PM + 1];
+#pragma unroll
+  for (int j = 0; j <= PM; ++j) b[j] = ld_coef(src, j, p);
+  l2l_shift<PM>(b, cplx{cx[gp] - cx[gc], cy[gp] - cy[gc]});       // parent - child
   double2* dst = local + gc * (p + 1);
 #pragma unroll
   for (int j = 0; j <= PM; ++j)
@@ -319,6 +328,45 @@ k_l2l(int l, long long c0, long long c1, const double* __restrict__ cx,
       double2 v = dst[j];
       dst[j] = make_double2(v.x + b[j].x, v.y + b[j].y);
     }
+}
+
+// Levels 2..lt of the L2L pass in ONE launch: a thread per level-lt box
+// walks its ancestor chain from level 1, re-computing every ancestor's
+// complete local expansion on the way (local[l+1][a] + shift(parent), the
+// same operations in the same order as the level-by-level kernel, so the
+// result is bit-identical) and writes the level-lt box's complete expansion.
+// The redundant ancestor work (~4x the few thousand shifts of these levels)
+// costs far less than the level-by-level launches it replaces, which are
+// pure latency at these sizes.
+template <int PM, bool EX>
+__global__ void __launch_bounds__(128)
+k_l2l_chain(int lt, const double* __restrict__ cx, const double* __restrict__ cy,
+            double2* local, int p) {
+  pdl_enter();
+  if constexpr (EX) p = PM;
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= (1ll << (2 * lt))) return;
+  cplx cur[PM + 1];
+  {
+    const long long g1 = level_base(1) + (b >> (2 * (lt - 1)));
+#pragma unroll
+    for (int j = 0; j <= PM; ++j) cur[j] = ld_coef(local + g1 * (p + 1), j, p);
+  }
+  for (int l = 1; l < lt; ++l) {
+    const long long gp = level_base(l) + (b >> (2 * (lt - l)));
+    const long long gc = level_base(l + 1) + (b >> (2 * (lt - l - 1)));
+    l2l_shift<PM>(cur, cplx{cx[gp] - cx[gc], cy[gp] - cy[gc]});
+    const double2* own = local + gc * (p + 1);
+#pragma unroll
+    for (int j = 0; j <= PM; ++j) {
+      const cplx v = ld_coef(own, j, p);
+      cur[j] = cplx{v.x + cur[j].x, v.y + cur[j].y};
+    }
+  }
+  double2* dst = local + (level_base(lt) + b) * (p + 1);
+#pragma unroll
+  for (int j = 0; j <= PM; ++j)
+    if (j <= p) dst[j] = make_double2(cur[j].x, cur[j].y);
 }
 
 // --------------------------------------------------------------------------
@@ -1102,7 +1150,23 @@ struct Launch {
                                            dstat);
   }
   static void l2l(const TreeState& T, ExpState& E, cudaStream_t st, const Part& part) {
-    for (int l = 1; l < T.L; ++l) {
+    int l_first = 1;
+    E.l2l_chain_lt = 0;
+    // single GPU: levels 2..lt (lt: the deepest level of at most 4096 boxes)
+    // through the chained kernel, the rest level by level
+    if (part.G == 1 && L2L_CHAIN) {
+      int lt = 1;
+      while (lt + 1 < T.L && (1ll << (2 * (lt + 1))) <= 4096) ++lt;
+      if (lt >= 3) {
+        note_launch();
+        launch(E.p == PM ? k_l2l_chain<PM, true> : k_l2l_chain<PM, false>,
+               nblk(1ll << (2 * lt), 128), 128, 0, st, lt, T.box_cx.as<double>(),
+               T.box_cy.as<double>(), E.local.as<double2>(), E.p);
+        l_first = lt;
+        E.l2l_chain_lt = lt;
+      }
+    }
+    for (int l = l_first; l < T.L; ++l) {
       const long long c0 = part.lo(l + 1), c1 = part.hi(l + 1);
       note_launch();
       launch(E.p == PM ? k_l2l<PM, true> : k_l2l<PM, false>, nblk(c1 - c0, 128), 128, 0, st, l,
@@ -1153,6 +1217,20 @@ void run_l2l(const TreeState& T, ExpState& E, DevStatus* dstat, cudaStream_t st,
   (void)dstat;
   dispatch_p(E.p, [&](auto pm) { Launch<decltype(pm)::value>::l2l(T, E, st, part); });
 }
+void complete_chained_locals(const TreeState& T, ExpState& E, double2* out, cudaStream_t st) {
+  const int lt = E.l2l_chain_lt;
+  if (lt < 3) return;
+  dispatch_p(E.p, [&](auto pm) {
+    constexpr int PM = decltype(pm)::value;
+    for (int l = 1; l + 1 < lt; ++l) {   // children at levels 2..lt-1, level by level
+      note_launch();
+      launch(E.p == PM ? k_l2l<PM, true> : k_l2l<PM, false>, nblk(1ll << (2 * (l + 1)), 128),
+             128, 0, st, l, 0ll, 1ll << (2 * (l + 1)), T.box_cx.as<double>(),
+             T.box_cy.as<double>(), out, E.p);
+    }
+  });
+}
+
 void run_l2p_m2p(const TreeState& T, const ListState& Ls, ExpState& E, DevStatus* dstat,
                  cudaStream_t st, long long e0, long long e1, long long leaf_range_lo,
                  long long leaf_range_hi) {

@@ -775,7 +775,18 @@ int fmm2d_export_expansions(fmm2d_ctx* c, double* mult, double* local) {
     if (!c->have_eval) throw ApiError{FMM2D_EBADARG, "no evaluation in this context"};
     const long long cnt = level_base(c->T.L + 1) * (c->E.p + 1);
     if (mult) FMM_CUDA(cudaMemcpy(mult, c->E.mult.p, sizeof(double2) * cnt, cudaMemcpyDeviceToHost));
-    if (local) FMM_CUDA(cudaMemcpy(local, c->E.local.p, sizeof(double2) * cnt, cudaMemcpyDeviceToHost));
+    if (local) {
+      // the chained L2L leaves the levels it passes through M2L-only: complete
+      // them level by level on a copy (same arithmetic as the engine's chain)
+      DBuf tmp;
+      tmp.reserve(sizeof(double2) * cnt);
+      FMM_CUDA(cudaMemcpyAsync(tmp.p, c->E.local.p, sizeof(double2) * cnt,
+                               cudaMemcpyDeviceToDevice, c->st));
+      complete_chained_locals(c->T, c->E, tmp.as<double2>(), c->st);
+      FMM_CUDA(cudaMemcpyAsync(local, tmp.p, sizeof(double2) * cnt, cudaMemcpyDeviceToHost,
+                               c->st));
+      FMM_CUDA(cudaStreamSynchronize(c->st));
+    }
     return FMM2D_OK;
   });
 }

@@ -26,8 +26,9 @@ constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 // near sources staged per warp per round: 256 for leaves of <= 32 points
 // (C2: ~210 near sources per leaf, one round), 512 for the two-block kernel
-// (C5: ~510 per leaf -- one round instead of two; 48 KB of SMEM per CTA;
-// measured C5 P2P 4.12 -> 3.88 ms, C2 unchanged with 256)
+// (C5: ~510 per leaf -- one staging round trip instead of two; 48 KB of SMEM
+// per CTA; measured C5 P2P 4.12 -> 3.88 ms, C2 unchanged with 256).  The
+// compute consumes every round in 256-source sub-chunks (same sums).
 constexpr int P2P_CHUNK1 = 256, P2P_CHUNK2 = 512;
 #ifndef P2P_SCAN
 #define P2P_SCAN 1
@@ -323,15 +324,24 @@ k_p2p(long long b0, long long b1, const int* __restrict__ soff, const int* __res
 #endif
       cp_async_wait_all();
       __syncwarp();
-      if (fast) {
-        if (active) p2p_slice<true>(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
-        // second block of points (leaves of 33..64 points): same staged chunk
-        if (DUAL && activeB)
-          p2p_slice<true>(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
-      } else {
-        if (active) p2p_slice<false>(sp, sg, fill * grp / G, fill * (grp + 1) / G, y, ax, ay, skips);
-        if (DUAL && activeB)
-          p2p_slice<false>(sp, sg, fill * grpB / GB, fill * (grpB + 1) / GB, yB, axB, ayB, skips);
+      // the staged round is consumed in sub-chunks of P2P_CHUNK1 sources: the
+      // slice boundaries, hence every point's summation order, are those of
+      // 256-source rounds whatever the staging size (bit-identical results)
+      for (int sub = 0; sub < fill; sub += P2P_CHUNK1) {
+        const int f = min(P2P_CHUNK1, fill - sub);
+        const double2* sps = sp + sub;
+        const double* sgs = sg + sub;
+        if (fast) {
+          if (active) p2p_slice<true>(sps, sgs, f * grp / G, f * (grp + 1) / G, y, ax, ay, skips);
+          // second block of points (leaves of 33..64 points): same staged chunk
+          if (DUAL && activeB)
+            p2p_slice<true>(sps, sgs, f * grpB / GB, f * (grpB + 1) / GB, yB, axB, ayB, skips);
+        } else {
+          if (active)
+            p2p_slice<false>(sps, sgs, f * grp / G, f * (grp + 1) / G, y, ax, ay, skips);
+          if (DUAL && activeB)
+            p2p_slice<false>(sps, sgs, f * grpB / GB, f * (grpB + 1) / GB, yB, axB, ayB, skips);
+        }
       }
       __syncwarp();
     }
