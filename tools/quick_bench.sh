@@ -2,7 +2,7 @@
 # quick check: GPU parity + engine tests, bench lines (phase times), optional ncu of a kernel
 TAG=${1:-q}; KRE=${2:-}; CFGS=${3:-"c2 c3 c5"}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_engine.py -x -q -m gpu > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_engine.py tests/test_gpu_headline.py -x -q -m gpu > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
 tail -2 $O/pytest.log
 for c in $CFGS; do
   timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $O/$c.json 2> $O/$c.err
