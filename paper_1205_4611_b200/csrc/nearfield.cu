@@ -99,11 +99,14 @@ __device__ __forceinline__ void p2p_term(double zx, double zy, double g, double 
   // r2 >= 0, so its high word is zero only for 0 or a denormal (which
   // rcp.approx.ftz cannot invert either): one 32-bit test selects the seed
   // of 1/1 instead; the Newton step then sees r2 = 0 and returns 3 y, a
-  // finite factor on dx = dy = 0.  The skip count is one predicated add.
+  // finite factor on dx = dy = 0.  The skip count (operators.py:266-274) is
+  // exactly r2 == 0: both words zero, one predicated add.
   int hi = __double2hiint(r2);
-  asm("{\n\t.reg .pred z;\n\tsetp.eq.s32 z, %1, 0;\n\t@z add.s32 %0, %0, 1;\n\t"
-      "selp.b32 %1, 1072693248, %1, z;\n\t}"
-      : "+r"(skips), "+r"(hi));
+  const int lo = __double2loint(r2);
+  asm("{\n\t.reg .pred z, c;\n\t.reg .b32 t;\n\tor.b32 t, %1, %2;\n\t"
+      "setp.eq.s32 c, t, 0;\n\t@c add.s32 %0, %0, 1;\n\t"
+      "setp.eq.s32 z, %1, 0;\n\tselp.b32 %1, 1072693248, %1, z;\n\t}"
+      : "+r"(skips), "+r"(hi) : "r"(lo));
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(__hiloint2double(hi, 0)));
   const double e = fma(-r2, y, 1.0);
