@@ -182,11 +182,20 @@ def _agreed(comm: Comm, fn):
     pairs -- then agree on the outcome: every rank raises the failure of the
     lowest failing rank (same exception type and message as the single-GPU
     engine), so no rank is left blocked in the next collective."""
+    import torch
     err = None
     try:
         out = fn()
     except (ValueError, MemoryError, _lib.EngineError) as e:   # DegenerateInputError is a ValueError
         err, out = e, None
+    # one tiny MAX allreduce decides whether anyone failed; only then are the
+    # messages gathered (pickled objects cost a host round trip per rank)
+    flag = torch.tensor([0 if err is None else 1], dtype=torch.int32)
+    if not comm.staged:
+        flag = flag.cuda()
+    comm.allreduce(flag, "max")
+    if int(flag.item()) == 0:
+        return out
     info = [None] * comm.size
     comm.dist.all_gather_object(info, None if err is None else (type(err).__name__, str(err)),
                                 group=comm.group)
