@@ -29,6 +29,9 @@ constexpr int M2P_INLINE = 16;
 #ifndef L2L_CHAIN
 #define L2L_CHAIN 1      // chained kernel for the small top levels of the L2L pass
 #endif
+#ifndef L2L_CHAIN_MAXBOX
+#define L2L_CHAIN_MAXBOX 4096   // deepest chained level: at most this many boxes
+#endif
    // m2p sources per point handled by k_l2p_m2p itself
 // M2L variant: dense Pascal-matrix kernel (default, PM <= 32) or the
 // target-owned lane-pair cascade (PM > 32, or FMM2D_M2L=target for A/B runs)
@@ -1156,7 +1159,7 @@ struct Launch {
     // through the chained kernel, the rest level by level
     if (part.G == 1 && L2L_CHAIN) {
       int lt = 1;
-      while (lt + 1 < T.L && (1ll << (2 * (lt + 1))) <= 4096) ++lt;
+      while (lt + 1 < T.L && (1ll << (2 * (lt + 1))) <= L2L_CHAIN_MAXBOX) ++lt;
       if (lt >= 3) {
         note_launch();
         launch(E.p == PM ? k_l2l_chain<PM, true> : k_l2l_chain<PM, false>,
