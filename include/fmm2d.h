@@ -127,6 +127,10 @@ int fmm2d_export_phi(fmm2d_ctx* ctx, double* phi_xy);
 /* replaces fmm2d.engine.direct_evaluate (engine.py:282-300), asymmetric mode */
 int fmm2d_direct(fmm2d_ctx* ctx, int64_t n, const double* pos_xy, const double* gamma,
                  int64_t m, const double* eval_xy, double* out_xy);
+/* replaces direct_evaluate(points, symmetric=True) (engine.py:302-323): evaluation
+ * points alias the n sources; each pairwise reciprocal serves both directions */
+int fmm2d_direct_symmetric(fmm2d_ctx* ctx, int64_t n, const double* pos_xy,
+                           const double* gamma, double* out_xy);
 
 /* ---------------------------------------------------------------------------
  * Unit operators (replace fmm2d.operators, operators.py:63-297) on the GPU.

@@ -68,6 +68,7 @@ _SIGS = {
     "fmm2d_export_expansions": (C.c_int, [C.c_void_p, _dp, _dp]),
     "fmm2d_export_phi": (C.c_int, [C.c_void_p, _dp]),
     "fmm2d_direct": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]),
+    "fmm2d_direct_symmetric": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, _dp]),
     # unit operators and per-level connectivity (operators.py, connectivity.py:47-96)
     "fmm2d_op_p2m": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _dp, _dp, _dp, C.c_int, _dp]),
     "fmm2d_op_p2l": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _dp, _dp, _dp, C.c_int, _dp]),

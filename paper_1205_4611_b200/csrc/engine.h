@@ -255,6 +255,10 @@ void run_stats(const TreeState& T, ListState& Ls, DevStatus* dstat, cudaStream_t
 
 void run_direct(const double2* src, const double* g, int64_t n, const double2* tgt, int64_t m,
                 double2* out, cudaStream_t st);
+// symmetric all-pairs direct sum (aliased points): W = double2[direct_sym_tiles(n) * n] scratch
+long long direct_sym_tiles(int64_t n, int64_t* st_out);
+void run_direct_symmetric(const double2* src, const double* g, int64_t n, double2* W,
+                          double2* out, cudaStream_t st);
 
 // device-wide exclusive scan of int32 counts: out[i] = *base + sum(in[0..i)),
 // out[n] = *base + total (base = 0 when null).  `tmp` is grown as needed.

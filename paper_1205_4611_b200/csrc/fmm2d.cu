@@ -827,4 +827,26 @@ int fmm2d_direct(fmm2d_ctx* c, int64_t n, const double* pos, const double* g, in
   });
 }
 
+int fmm2d_direct_symmetric(fmm2d_ctx* c, int64_t n, const double* pos, const double* g,
+                           double* out) {
+  if (!c) return FMM2D_EBADARG;
+  return guarded(c, [&] {
+    validate(n, n, 1, 0.5, 1, false);
+    FMM_CUDA(cudaSetDevice(c->device));
+    DBuf dp, dg, dw, dout;
+    dp.reserve(sizeof(double2) * n);
+    dg.reserve(sizeof(double) * n);
+    dout.reserve(sizeof(double2) * n);
+    dw.reserve(sizeof(double2) * n * direct_sym_tiles(n, nullptr));
+    FMM_CUDA(cudaMemcpyAsync(dp.p, pos, sizeof(double2) * n, cudaMemcpyHostToDevice, c->st));
+    FMM_CUDA(cudaMemcpyAsync(dg.p, g, sizeof(double) * n, cudaMemcpyHostToDevice, c->st));
+    run_direct_symmetric(dp.as<double2>(), dg.as<double>(), n, dw.as<double2>(),
+                         dout.as<double2>(), c->st);
+    FMM_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->st));
+    FMM_CUDA(cudaStreamSynchronize(c->st));
+    FMM_CUDA(cudaGetLastError());
+    return FMM2D_OK;
+  });
+}
+
 }  // extern "C"

@@ -409,6 +409,144 @@ k_direct(const double2* __restrict__ src, const double* __restrict__ g, long lon
   if (t < m) out[t] = make_double2(ax, -ay);
 }
 
+// Symmetric direct sum (engine.py:302-323, evaluation points aliasing the
+// sources): every unordered pair shares one reciprocal between its two
+// directions, 13 FP64 instructions per pair instead of 2 x 10.  The point
+// set is cut into nbs super-tiles of ST points; CTA (I, J), I < J, sums J
+// into I's points and I into J's, CTA (I, I) sums its tile asymmetrically.
+// Each CTA writes its partial potentials into its own slots of W[nbs][n]
+// (W[J][i]: super-tile J's contribution to point i), and k_direct_fold adds
+// a point's nbs slots in ascending J: deterministic, no atomics.
+//
+// Inside a CTA (8 warps, one i per thread): a 256-point j-chunk is staged in
+// SMEM; in 8 sub-steps warp w takes j-block (w + s) & 7, so each j-block is
+// owned by one warp at a time.  Lane l pairs its i with j = (l + k) & 31 at
+// step k and holds that j's accumulator, handed one lane down after the
+// step (lane l + 1's j is lane l's next): j's terms arrive in a fixed order.
+// The reciprocal is the P2P's (rcp.approx seed, one cubic Newton step;
+// r2 == 0 gives a finite seed and dx == dy == 0, so a coincident pair adds
+// exact zeros, the reference's skip).
+constexpr int DSYM_THREADS = 256;
+#ifndef DSYM_NI
+#define DSYM_NI 2           // i's per thread
+#endif
+#ifndef DSYM_MAX_TILES
+#define DSYM_MAX_TILES 128
+#endif
+
+__device__ __forceinline__ double rcp_r2(double r2) {
+  double y;
+  asm("{\n\t.reg .b32 h, q, h2, q2;\n\t.reg .b64 s, t;\n\t"
+      "mov.b64 {q, h}, %1;\n\t"
+      "max.s32 h, h, 0x2d000000;\n\t"
+      "mov.b64 s, {q, h};\n\t"
+      "rcp.approx.ftz.f64 t, s;\n\t"
+      "mov.b64 {q2, h2}, t;\n\t"
+      "mov.b64 %0, {h, h2};\n\t}"
+      : "=d"(y) : "d"(r2));
+  const double e = fma(-r2, y, 1.0);
+  return fma(fma(e, e, e), y, y);
+}
+
+__global__ void __launch_bounds__(DSYM_THREADS)
+k_direct_sym(const double2* __restrict__ z, const double* __restrict__ g, long long n,
+             long long ST, double2* __restrict__ W) {
+  pdl_enter();
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (J < I) return;
+  __shared__ double2 s_z[DSYM_THREADS];
+  __shared__ double s_g[DSYM_THREADS];
+  __shared__ double2 s_acc[DSYM_THREADS];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long I0 = I * ST, I1 = min(n, I0 + ST), J0 = J * ST, J1 = min(n, J0 + ST);
+  // DSYM_NI i's per thread (i-chunk DSYM_NI * 256): each staged j and each
+  // accumulator hand-off serves DSYM_NI pairs
+  for (long long ic = I0; ic < I1; ic += DSYM_NI * DSYM_THREADS) {
+    double2 zi[DSYM_NI];
+    double gi[DSYM_NI], ax[DSYM_NI], ay[DSYM_NI];
+#pragma unroll
+    for (int u = 0; u < DSYM_NI; ++u) {
+      const long long i = ic + u * DSYM_THREADS + tid;
+      zi[u] = i < I1 ? z[i] : make_double2(0.0, 0.0);
+      gi[u] = i < I1 ? g[i] : 0.0;
+      ax[u] = ay[u] = 0.0;
+    }
+    for (long long jc = J0; jc < J1; jc += DSYM_THREADS) {
+      const long long j = jc + tid;
+      const bool vj = j < J1;
+      __syncthreads();
+      s_z[tid] = vj ? z[j] : make_double2(0.0, 0.0);
+      s_g[tid] = vj ? g[j] : 0.0;
+      if (I != J) s_acc[tid] = (ic == I0 || !vj) ? make_double2(0.0, 0.0)
+                                                 : W[(long long)I * n + j];
+      __syncthreads();
+      if (I == J) {
+        // diagonal super-tile: asymmetric, each i over the whole chunk
+#pragma unroll
+        for (int u = 0; u < DSYM_NI; ++u) {
+          double bx = 0.0, by = 0.0;
+#pragma unroll 4
+          for (int k = 0; k < DSYM_THREADS; ++k) {
+            const double2 zj = s_z[k];
+            const double dx = zj.x - zi[u].x, dy = zj.y - zi[u].y;
+            const double y = rcp_r2(fma(dx, dx, dy * dy)) * s_g[k];
+            bx = fma(y, dx, bx);
+            by = fma(y, dy, by);
+          }
+          ax[u] += bx;
+          ay[u] += by;
+        }
+        continue;
+      }
+      for (int sb = 0; sb < 8; ++sb) {
+        const int base = ((wid + sb) & 7) * 32;
+        double2 aj = s_acc[base + lane];
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const int jj = base + ((lane + k) & 31);
+          const double2 zj = s_z[jj];
+          const double gj = s_g[jj];
+#pragma unroll
+          for (int u = 0; u < DSYM_NI; ++u) {
+            const double dx = zj.x - zi[u].x, dy = zj.y - zi[u].y;
+            const double y = rcp_r2(fma(dx, dx, dy * dy));
+            const double re = dx * y, im = dy * y;
+            ax[u] = fma(gj, re, ax[u]);
+            ay[u] = fma(gj, im, ay[u]);
+            aj.x = fma(-gi[u], re, aj.x);
+            aj.y = fma(-gi[u], im, aj.y);
+          }
+          aj.x = __shfl_sync(0xffffffffu, aj.x, lane + 1);
+          aj.y = __shfl_sync(0xffffffffu, aj.y, lane + 1);
+        }
+        s_acc[base + lane] = aj;
+        __syncthreads();
+      }
+      if (vj) W[(long long)I * n + j] = s_acc[tid];
+    }
+#pragma unroll
+    for (int u = 0; u < DSYM_NI; ++u) {
+      const long long i = ic + u * DSYM_THREADS + tid;
+      if (i < I1) W[(long long)J * n + i] = make_double2(ax[u], ay[u]);
+    }
+  }
+}
+
+// phi_i = sum over super-tiles J (ascending) of W[J][i]; conjugate at the end
+__global__ void k_direct_fold(const double2* __restrict__ W, long long n, int nbs,
+                              double2* __restrict__ out) {
+  pdl_enter();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ax = 0.0, ay = 0.0;
+  for (int J = 0; J < nbs; ++J) {
+    const double2 v = W[(long long)J * n + i];
+    ax += v.x;
+    ay += v.y;
+  }
+  out[i] = make_double2(ax, -ay);
+}
+
 inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -440,6 +578,29 @@ void run_direct(const double2* src, const double* g, int64_t n, const double2* t
                 double2* out, cudaStream_t st) {
   note_launch();
   launch(k_direct, nblk(m, DIRECT_TILE), DIRECT_TILE, 0, st, src, g, n, tgt, m, out);
+}
+
+long long direct_sym_tiles(int64_t n, int64_t* st_out) {
+  // super-tiles: a multiple of the i-chunk, >= 512 points, at most
+  // DSYM_MAX_TILES of them (up to 8256 CTAs of equal work; W costs
+  // n * nbs * 16 bytes)
+  constexpr long long CH = DSYM_NI * DSYM_THREADS;
+  const long long ST = std::max<long long>(
+      512, ((n + DSYM_MAX_TILES - 1) / DSYM_MAX_TILES + CH - 1) / CH * CH);
+  if (st_out) *st_out = ST;
+  return (n + ST - 1) / ST;
+}
+
+void run_direct_symmetric(const double2* src, const double* g, int64_t n, double2* W,
+                          double2* out, cudaStream_t st) {
+  if (n <= 0) return;
+  int64_t ST = 0;
+  const long long nbs = direct_sym_tiles(n, &ST);
+  note_launch();
+  launch(k_direct_sym, dim3((unsigned)nbs, (unsigned)nbs), DSYM_THREADS, 0, st, src, g,
+         (long long)n, (long long)ST, W);
+  note_launch();
+  launch(k_direct_fold, nblk(n, 256), 256, 0, st, W, (long long)n, (int)nbs, out);
 }
 
 }  // namespace fmm

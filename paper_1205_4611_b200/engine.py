@@ -170,17 +170,25 @@ def direct_evaluate(points: ParticleSet, symmetric: bool = False, *,
                     device: int | None = None) -> np.ndarray:
     """All-pairs direct sum on the GPU (replaces engine.py:282-323).
 
-    ``symmetric=True`` keeps the reference's contract (evaluation points
-    must alias the sources); the GPU evaluates both modes with the same
-    asymmetric kernel, which the reference matches to roundoff.
+    Asymmetric mode (engine.py:291-300): thread per evaluation point, IEEE
+    ``1/r2`` as in ``reciprocal_parts`` (operators.py:258-277).  Symmetric
+    mode (engine.py:302-323) requires aliased evaluation points, like the
+    reference, and shares each pairwise reciprocal between both directions
+    (``k_direct_sym``: super-tile pairs, deterministic fold); it matches the
+    asymmetric mode to roundoff, as the reference's does.
     """
     if symmetric and not points.evals_alias_sources:
         raise ValueError("symmetric mode requires evaluation points to alias the sources")
     ctx = _lib.default_context(device)
     pos = points.positions
-    epos = None if points.evals_alias_sources else points.eval_positions
     out = np.empty(points.n_evals, np.complex128)
     with ctx.lock:
+        if symmetric:
+            ctx.check(ctx.lib.fmm2d_direct_symmetric(
+                ctx.h, pos.size, _lib.dptr(pos.view(np.float64)), _lib.dptr(points.strengths),
+                _lib.dptr(out.view(np.float64))))
+            return out
+        epos = None if points.evals_alias_sources else points.eval_positions
         ctx.check(ctx.lib.fmm2d_direct(
             ctx.h, pos.size, _lib.dptr(pos.view(np.float64)), _lib.dptr(points.strengths),
             points.n_evals, None if epos is None else _lib.dptr(epos.view(np.float64)),

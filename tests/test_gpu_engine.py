@@ -32,6 +32,51 @@ def test_direct_symmetric_requires_aliasing():
         F.direct_evaluate(pts, symmetric=True)
 
 
+GOLD_DIRECT = ["uniform_3000", "normal_dup_2701"]
+
+
+@pytest.mark.parametrize("name", GOLD_DIRECT)
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_direct_matches_reference_goldens(name, symmetric):
+    """Both modes against the reference's own direct_evaluate outputs
+    (tests/golden/make_golden_direct.py); normal_dup has exact duplicates."""
+    from helpers import load
+    d = load("direct_sum")
+    pts = F.ParticleSet(d[f"{name}_positions"], d[f"{name}_strengths"])
+    want = d[f"{name}_symmetric" if symmetric else f"{name}_asymmetric"]
+    got = F.direct_evaluate(pts, symmetric=symmetric)
+    assert F.max_rel_error(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 2, 255, 513, 70_001])
+def test_direct_symmetric_equals_asymmetric(n):
+    """Ragged super-tiles and chunks: the shared-reciprocal sum agrees with the
+    asymmetric one to roundoff, and is deterministic run to run."""
+    pts = uniform(n, seed=21)
+    sym = F.direct_evaluate(pts, symmetric=True)
+    asym = F.direct_evaluate(pts)
+    if n == 1:
+        assert sym[0] == 0 and asym[0] == 0
+        return
+    # two different summation orders over n terms: compare against the size of
+    # the terms, |dphi_i| / sum_j |g_j / (z_j - z_i)| (a plain relative bound
+    # grows with n where cancellation makes |phi_i| small)
+    import torch
+    dev = torch.device("cuda", 0)
+    z = torch.from_numpy(pts.positions).to(dev)
+    g = torch.from_numpy(np.abs(pts.strengths)).to(dev)
+    scale = torch.empty(n, dtype=torch.float64, device=dev)
+    for s0 in range(0, n, 256):
+        d = torch.abs(z[None, :] - z[s0:s0 + 256, None])
+        t = g[None, :] / d
+        t[d == 0] = 0.0
+        scale[s0:s0 + 256] = t.sum(dim=1)
+    cond = np.abs(sym - asym) / scale.cpu().numpy()
+    assert cond.max() <= 1e-15 * max(1.0, np.sqrt(n) / 16)
+    assert F.max_rel_error(sym, asym) <= 1e-11
+    assert np.array_equal(sym, F.direct_evaluate(pts, symmetric=True))
+
+
 def test_direct_separate_eval_points():
     pts = F.ParticleSet(np.array([0j, 1.0 + 0j]), np.array([2.0, -1.0]),
                         np.array([0.5 + 0j, 3.0 + 0j]))

@@ -82,3 +82,13 @@ def test_oracle_direct_small_cases():
 def test_oracle_degenerate():
     with pytest.raises(O.OracleDegenerate, match="coincide"):
         O.build_tree(np.full(10, 0.5 + 0.5j), np.ones(10), None, 1)
+
+
+@pytest.mark.parametrize("name", ["uniform_3000", "normal_dup_2701"])
+def test_oracle_direct_matches_reference(name):
+    """The oracle's direct sum against the reference's direct_evaluate in both
+    modes (tests/golden/make_golden_direct.py); duplicates contribute nothing."""
+    d = load("direct_sum")
+    phi = O.direct(d[f"{name}_positions"], d[f"{name}_strengths"])
+    assert O.max_rel(phi, d[f"{name}_asymmetric"]) <= 1e-13
+    assert O.max_rel(phi, d[f"{name}_symmetric"]) <= 1e-12
