@@ -26,6 +26,9 @@ struct DistState {
   std::vector<std::vector<long long>> off;     // data-independent offsets, steps 0..2L
   std::vector<std::vector<double>> rect;       // top split: 4 doubles per segment, steps 0..s0
   DBuf leaf_off;                               // int32 [4^L + 1] global leaf offsets
+  long long off_key_n = -1;                   // (n_total, L) of off / leaf_off
+  int off_key_L = -1;
+  DBuf totals5;                                // list totals for the report
   DBuf rec_a, rec_b;                           // top-split records {x, y, g, idx}
   long long n_local = 0;                       // records held before the exchange
   std::vector<long long> seg_off;              // local record offsets per top segment

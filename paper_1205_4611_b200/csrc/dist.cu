@@ -347,6 +347,25 @@ __global__ void k_owner_keys(const int* __restrict__ nsel, const int* __restrict
   keys[i] = leaf_level >= 0 ? (unsigned)(id >> (2 * leaf_level - s0)) : (unsigned)owner_of(id, s0);
 }
 
+// requests per owner q < G from the owner-sorted keys (binary search)
+__global__ void k_owner_counts(const int* __restrict__ nsel, const unsigned* __restrict__ keys,
+                               int G, int* counts) {
+  pdl_enter();
+  const int q = threadIdx.x;
+  if (q >= G) return;
+  const int n = *nsel;
+  auto lower = [&](unsigned v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  counts[q] = lower((unsigned)q + 1) - lower((unsigned)q);
+}
+
 // -------------------------------------------------------------------------
 // halo payloads
 // particles: every requested leaf travels as nmax records {x, y, g} (padded)
@@ -470,6 +489,18 @@ __global__ void k_eoff_global(long long nleaf, long long b0, long long nl,
   out[b] = b < b0 ? 0 : (b > b0 + nl ? m : loc[b - b0]);
 }
 
+__global__ void k_pick5(const int* a, const int* b, const int* c, const int* d, const int* e,
+                        int* out) {
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    out[0] = *a;
+    out[1] = *b;
+    out[2] = *c;
+    out[3] = *d;
+    out[4] = *e;
+  }
+}
+
 __global__ void k_add_base(long long m, const unsigned* __restrict__ in, unsigned base,
                            unsigned* out) {
   pdl_enter();
@@ -566,23 +597,24 @@ int fmm2d_dist_setup(fmm2d_ctx* c, int G, int rank, int64_t n_total, int p, doub
     D.nd = nd;
     if (2 * D.L < D.part.s0)
       throw ApiError{FMM2D_EBADARG, "too few points for this many ranks (need 4^levels >= ranks)"};
-    // data-independent offsets of every global step (tree.py:308-310)
+    // data-independent offsets of every global step (tree.py:308-310): kept
+    // (host tables and the device leaf offsets) while (n_total, L) repeat
     const int S = 2 * D.L;
-    D.off.assign(S + 1, {});
-    D.off[0] = {0, n_total};
-    for (int s = 0; s < S; ++s) {
-      const auto& o = D.off[s];
-      std::vector<long long> nx(2 * (o.size() - 1) + 1);
-      nx[0] = 0;
-      for (size_t j = 0; j + 1 < o.size(); ++j) {
-        const long long cnt = o[j + 1] - o[j];
-        nx[2 * j + 1] = o[j] + (cnt + 1) / 2;
-        nx[2 * j + 2] = o[j + 1];
-      }
-      D.off[s + 1] = std::move(nx);
-    }
     const long long nleaf = 1ll << S;
-    {
+    if (D.off_key_n != n_total || D.off_key_L != D.L || D.leaf_off.p == nullptr) {
+      D.off.assign(S + 1, {});
+      D.off[0] = {0, n_total};
+      for (int s = 0; s < S; ++s) {
+        const auto& o = D.off[s];
+        std::vector<long long> nx(2 * (o.size() - 1) + 1);
+        nx[0] = 0;
+        for (size_t j = 0; j + 1 < o.size(); ++j) {
+          const long long cnt = o[j + 1] - o[j];
+          nx[2 * j + 1] = o[j] + (cnt + 1) / 2;
+          nx[2 * j + 2] = o[j + 1];
+        }
+        D.off[s + 1] = std::move(nx);
+      }
       std::vector<int> lo(nleaf + 1);
       long long mx = 0;
       for (long long k = 0; k <= nleaf; ++k) lo[k] = (int)D.off[S][k];
@@ -593,6 +625,8 @@ int fmm2d_dist_setup(fmm2d_ctx* c, int G, int rank, int64_t n_total, int p, doub
       FMM_CUDA(cudaMemcpyAsync(D.leaf_off.p, lo.data(), sizeof(int) * (nleaf + 1),
                                cudaMemcpyHostToDevice, c->st));
       sync(c);
+      D.off_key_n = n_total;
+      D.off_key_L = D.L;
     }
     D.g0 = D.off[D.part.s0][rank];
     D.n_r = D.off[D.part.s0][rank + 1] - D.g0;
@@ -1129,41 +1163,56 @@ int fmm2d_dist_connect(fmm2d_ctx* c, const double* d_geo_all, int64_t* req_count
     note_launch();
     launch(k_mark_leaf_lists, nblk((b1 - b0) * 32, 256), 256, 0, c->st, 
         b0, b1, Ls.p2l_off.as<int>(), Ls.p2l_idx.as<int>(), tshift, rank, 0, fl);
+    // both kinds: flagged ids (boxes at offset 0, leaves at nbox), one count
+    // read-back, owner-grouped ids (stable sort by owner key), per-owner
+    // request counts on the device, one read-back
+    const long long nn[2] = {nbox, nleaf}, base[2] = {0, nbox};
+    D.ids.reserve(sizeof(int) * (nbox + nleaf));
+    D.keys.reserve(sizeof(unsigned) * (nbox + nleaf));
+    D.keys_sorted.reserve(sizeof(unsigned) * (nbox + nleaf));
+    D.nsel.reserve(sizeof(int) * (4 + 2 * 64));
+    int* nsel_d = D.nsel.as<int>();
+    int* cnt_d = nsel_d + 4;
     for (int kind = 0; kind < 2; ++kind) {
-      const long long nn = kind == 0 ? nbox : nleaf;
       const unsigned char* f = kind == 0 ? fb : fl;
-      D.ids.reserve(sizeof(int) * nn);
-      D.keys.reserve(sizeof(unsigned) * nn);
-      D.keys_sorted.reserve(sizeof(unsigned) * nn);
-      D.nsel.reserve(sizeof(int) * 4);
       size_t bytes = 0;
       cub::CountingInputIterator<int> it(0);
-      FMM_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, f, D.ids.as<int>(),
-                                          D.nsel.as<int>(), (int)nn, c->st));
+      FMM_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, f, D.ids.as<int>() + base[kind],
+                                          nsel_d + kind, (int)nn[kind], c->st));
       D.cub_tmp.reserve(bytes);
-      FMM_CUDA(cub::DeviceSelect::Flagged(D.cub_tmp.p, bytes, it, f, D.ids.as<int>(),
-                                          D.nsel.as<int>(), (int)nn, c->st));
-      int nsel = 0;
-      FMM_CUDA(cudaMemcpyAsync(&nsel, D.nsel.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-      sync(c);
-      D.req_ids[kind].reserve(sizeof(int) * std::max(1, nsel));
-      std::vector<unsigned> keys(nsel);
-      if (nsel > 0) {
+      FMM_CUDA(cub::DeviceSelect::Flagged(D.cub_tmp.p, bytes, it, f,
+                                          D.ids.as<int>() + base[kind], nsel_d + kind,
+                                          (int)nn[kind], c->st));
+    }
+    int nsel[2] = {0, 0};
+    FMM_CUDA(cudaMemcpyAsync(nsel, nsel_d, sizeof nsel, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    int bits = 1;
+    while ((1 << bits) < G) ++bits;
+    for (int kind = 0; kind < 2; ++kind) {
+      D.req_ids[kind].reserve(sizeof(int) * std::max(1, nsel[kind]));
+      if (nsel[kind] > 0) {
         note_launch();
-        launch(k_owner_keys, nblk(nsel, 256), 256, 0, c->st, D.nsel.as<int>(), D.ids.as<int>(), s0,
-                                                         kind == 0 ? -1 : L,
-                                                         D.keys.as<unsigned>());
-        int bits = 1;
-        while ((1 << bits) < G) ++bits;
-        sort_pairs(D.cub_tmp, D.keys.as<unsigned>(), D.keys_sorted.as<unsigned>(),
-                   D.ids.as<int>(), D.req_ids[kind].as<int>(), nsel, bits, c->st);
-        FMM_CUDA(cudaMemcpyAsync(keys.data(), D.keys_sorted.p, sizeof(unsigned) * nsel,
-                                 cudaMemcpyDeviceToHost, c->st));
-        sync(c);
+        launch(k_owner_keys, nblk(nsel[kind], 256), 256, 0, c->st, nsel_d + kind,
+               D.ids.as<int>() + base[kind], s0, kind == 0 ? -1 : L,
+               D.keys.as<unsigned>() + base[kind]);
+        sort_pairs(D.cub_tmp, D.keys.as<unsigned>() + base[kind],
+                   D.keys_sorted.as<unsigned>() + base[kind], D.ids.as<int>() + base[kind],
+                   D.req_ids[kind].as<int>(), nsel[kind], bits, c->st);
       }
+      note_launch();
+      launch(k_owner_counts, 1, 64, 0, c->st, nsel_d + kind,
+             D.keys_sorted.as<unsigned>() + base[kind], G, cnt_d + kind * 64);
+    }
+    int cnt_h[2 * 64];
+    FMM_CUDA(cudaMemcpyAsync(cnt_h, cnt_d, sizeof(int) * 2 * 64, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int kind = 0; kind < 2; ++kind) {
       D.req_count[kind].assign(G, 0);
-      for (unsigned k : keys) D.req_count[kind][k]++;
-      for (int q = 0; q < G; ++q) req_counts[kind * G + q] = D.req_count[kind][q];
+      for (int q = 0; q < G; ++q) {
+        D.req_count[kind][q] = cnt_h[kind * 64 + q];
+        req_counts[kind * G + q] = cnt_h[kind * 64 + q];
+      }
     }
     c->have_lists = true;
     return FMM2D_OK;
@@ -1338,12 +1387,23 @@ int fmm2d_dist_downward(fmm2d_ctx* c, double* d_vals, int64_t* d_idx, fmm2d_repo
       const long long nbox = level_base(L + 1), nleaf = 1ll << (2 * L);
       int tw = 0, sh = 0, tp[3] = {0, 0, 0};
       const int lt = D.part.ltop();
-      FMM_CUDA(cudaMemcpy(&tw, Ls.weak_off.as<int>() + nbox, sizeof(int), cudaMemcpyDeviceToHost));
-      FMM_CUDA(cudaMemcpy(&sh, Ls.weak_off.as<int>() + level_base(lt), sizeof(int),
-                          cudaMemcpyDeviceToHost));
-      FMM_CUDA(cudaMemcpy(&tp[0], Ls.p2p_off.as<int>() + nleaf, sizeof(int), cudaMemcpyDeviceToHost));
-      FMM_CUDA(cudaMemcpy(&tp[1], Ls.p2l_off.as<int>() + nleaf, sizeof(int), cudaMemcpyDeviceToHost));
-      FMM_CUDA(cudaMemcpy(&tp[2], Ls.m2p_off.as<int>() + nleaf, sizeof(int), cudaMemcpyDeviceToHost));
+      {
+        // the five list totals in one kernel + one copy (the stream is idle here)
+        D.totals5.reserve(sizeof(int) * 8);
+        note_launch();
+        launch(k_pick5, 1, 32, 0, c->st, Ls.weak_off.as<int>() + nbox,
+               Ls.weak_off.as<int>() + level_base(lt), Ls.p2p_off.as<int>() + nleaf,
+               Ls.p2l_off.as<int>() + nleaf, Ls.m2p_off.as<int>() + nleaf,
+               D.totals5.as<int>());
+        int v[5];
+        FMM_CUDA(cudaMemcpyAsync(v, D.totals5.p, sizeof v, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        tw = v[0];
+        sh = v[1];
+        tp[0] = v[2];
+        tp[1] = v[3];
+        tp[2] = v[4];
+      }
       // weak pairs of shared targets are computed by every rank: count them on rank 0
       r.list_totals[0] = tw - (D.part.rank == 0 ? 0 : sh);
       r.list_totals[1] = tp[0];

@@ -61,6 +61,9 @@ class Comm:
         self.size = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.staged = dist.get_backend(group) != "nccl"
+        # a one-rank group exchanges with itself only: every collective is a
+        # local copy (no NCCL launch, no host round trip)
+        self.solo = self.size == 1
 
     def _host(self, t):
         return t.cpu() if self.staged and t.is_cuda else t
@@ -72,6 +75,8 @@ class Comm:
     def allreduce(self, t, op: str = "sum"):
         ops = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN,
                "max": self.dist.ReduceOp.MAX}
+        if self.solo:
+            return t
         h = self._host(t)
         self.dist.all_reduce(h, op=ops[op], group=self.group)
         self._back(h, t)
@@ -79,6 +84,10 @@ class Comm:
 
     def all_gather(self, out, inp):
         """out: ``size`` equal chunks along dim 0, rank order."""
+        if self.solo:
+            if out.data_ptr() != inp.data_ptr():
+                out.copy_(inp.reshape(out.shape))
+            return out
         hi = self._host(inp)
         if self.staged:
             chunks = [hi.new_empty(hi.shape) for _ in range(self.size)]
@@ -97,6 +106,10 @@ class Comm:
         """all-to-all with row counts per peer (rank order)."""
         out_splits = [int(v) for v in out_splits]
         in_splits = [int(v) for v in in_splits]
+        if self.solo:
+            if out.numel():
+                out.copy_(inp)
+            return out
         if self.staged:
             import torch
             hi = self._host(inp)
@@ -130,21 +143,41 @@ class Comm:
     def exchange_counts(self, counts):
         """counts[q] = items this rank sends to q -> items q sends to this rank."""
         import torch
+        if self.solo:
+            return [int(v) for v in counts]
         t = torch.tensor([int(v) for v in counts], dtype=torch.int64)
-        rows = torch.empty(self.size * self.size, dtype=torch.int64)
         if self.staged:
             chunks = [torch.empty_like(t) for _ in range(self.size)]
             self.dist.all_gather(chunks, t, group=self.group)
             rows = torch.stack(chunks)
         else:
-            dev = torch.device("cuda", torch.cuda.current_device())
-            g = torch.empty(self.size * self.size, dtype=torch.int64, device=dev)
-            self.dist.all_gather_into_tensor(g, t.to(dev), group=self.group)
-            rows = g.cpu().view(self.size, self.size)
+            # pinned staging both ways, one stream sync (the caller needs the
+            # sizes on the host anyway)
+            hin, hout, g = _pinned_counts(self.size)
+            hin.copy_(t)
+            self.dist.all_gather_into_tensor(g, hin.to(g.device, non_blocking=True),
+                                             group=self.group)
+            hout.copy_(g, non_blocking=True)
+            torch.cuda.current_stream(g.device).synchronize()
+            rows = hout.view(self.size, self.size)
         return [int(v) for v in rows[:, self.rank]]
 
 
 _streams: dict = {}
+_pinned: dict = {}
+
+
+def _pinned_counts(size: int):
+    """(pinned send row, pinned receive matrix, device matrix) for exchange_counts."""
+    import torch
+    dev = torch.cuda.current_device()
+    key = (dev, size)
+    if key not in _pinned:
+        _pinned[key] = (torch.empty(size, dtype=torch.int64).pin_memory(),
+                        torch.empty(size * size, dtype=torch.int64).pin_memory(),
+                        torch.empty(size * size, dtype=torch.int64,
+                                    device=torch.device("cuda", dev)))
+    return _pinned[key]
 
 
 def engine_stream(device: int):
@@ -183,6 +216,8 @@ def _agreed(comm: Comm, fn):
     lowest failing rank (same exception type and message as the single-GPU
     engine), so no rank is left blocked in the next collective."""
     import torch
+    if comm.solo:
+        return fn()
     err = None
     try:
         out = fn()
