@@ -2,6 +2,7 @@
 bytes, occupancy, issue activity, pipe use and the top stall reasons.
 
     python tools/ncu_multi.py report.ncu-rep > summary.txt
+    python tools/ncu_multi.py report_raw.csv > summary.txt   (ncu -i ... --page raw --csv)
 """
 import csv
 import io
@@ -22,13 +23,17 @@ COLS = [
     ("grid", "launch__grid_size", 1),
     ("block", "launch__block_size", 1),
 ]
-UNIT = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
-        "Gbyte": 1e9}
+UNIT = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "ns": 1, "us": 1e3, "ms": 1e6,
+        "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6,
+        "GB": 1e9}
 
 
 def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):          # an exported raw page
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units, data = rows[0], rows[1], rows[2:]
     idx = {k: i for i, k in enumerate(h)}
