@@ -425,6 +425,30 @@ constexpr M2LTab<PM> make_m2l_tab() {
 }
 template <int PM>
 __constant__ __align__(16) M2LTab<PM> c_m2l_tab = make_m2l_tab<PM>();
+#ifndef M2L_IMM
+#define M2L_IMM 1
+#endif
+// C(n, k) as a constant expression.  With compile-time (j, k) -- the exact-
+// order instantiations -- every coefficient below 2^21 becomes a DFMA
+// immediate (its low word is zero) and the rest a pair of uniform moves: no
+// constant-bank loads in the contraction (C2 M2L -0.9 %, C4 -2.5 %,
+// bit-identical; M2L_IMM=0 keeps the table form)
+__host__ __device__ constexpr double m2l_binom(int n, int k) {
+  unsigned long long c = 1;
+  for (int i = 1; i <= k; ++i) c = c * (unsigned long long)(n - k + i) / (unsigned long long)i;
+  return (double)c;
+}
+// compile-time j, k: the coefficient is a constant expression
+template <int PM, int J, int K>
+__device__ __forceinline__ void m2l_chain(double& sx, double& sy, const double* ax,
+                                          const double* ay) {
+  if constexpr (K <= PM) {
+    constexpr double cf = m2l_binom(J + K - 1, K - 1);
+    sx = fma(cf, ax[K - 1], sx);
+    sy = fma(cf, ay[K - 1], sy);
+    m2l_chain<PM, J, K + 1>(sx, sy, ax, ay);
+  }
+}
 
 template <int PM>
 struct M2LDenseCfg {
@@ -451,6 +475,25 @@ __device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
   if (set_flags && j == 0 && comp == 0) {
     const unsigned f = starts_before ? (ends_after ? 5u : 1u) : 2u;
     atomicOr(reinterpret_cast<unsigned int*>(item_flags + (item & ~3ll)), f << (8 * (item & 3)));
+  }
+}
+
+// exact-order contraction with compile-time (j, k): every output's chain in
+// the order of the table form, coefficients as constant expressions
+template <int PM, int J, int STR>
+__device__ __forceinline__ void m2l_outputs(const double* ax, const double* ay, cplx pw, cplx inv,
+                                            double* red, int tid) {
+  if constexpr (J <= PM) {
+    double sx = ax[0], sy = ay[0];
+    m2l_chain<PM, J, 2>(sx, sy, ax, ay);
+    cplx b{sx, sy};
+    if constexpr (J > 0) {
+      b = cmul(b, pw);
+      pw = cmul(pw, inv);
+    }
+    red[(2 * J) * STR + tid] = b.x;
+    red[(2 * J + 1) * STR + tid] = b.y;
+    m2l_outputs<PM, J + 1, STR>(ax, ay, pw, inv, red, tid);
   }
 }
 
@@ -562,6 +605,11 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
       }
     }
     // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
+#if M2L_IMM
+    if constexpr (EX) {
+      m2l_outputs<PM, 0, Cfg::STR>(ax, ay, inv, inv, red, tid);
+    } else
+#endif
     {
       cplx pw = inv;
 #pragma unroll
