@@ -425,6 +425,9 @@ constexpr M2LTab<PM> make_m2l_tab() {
 }
 template <int PM>
 __constant__ __align__(16) M2LTab<PM> c_m2l_tab = make_m2l_tab<PM>();
+#ifndef M2L_HALF
+#define M2L_HALF 1
+#endif
 #ifndef M2L_IMM
 #define M2L_IMM 1
 #endif
@@ -455,6 +458,13 @@ struct M2LDenseCfg {
   static constexpr int R = 2 * (PM + 1);          // SMEM rows (re/im per coefficient)
   static constexpr int STR = M2L_ITEM + 1;        // odd row stride: conflict-free
   static constexpr int SMEM = R * STR * 8;
+  // exact orders above 20 (M2L_HALF): outputs j <= JH are parked and folded
+  // first, then the rest in the same rows -- half the SMEM, so more L1 for
+  // the source rows that consecutive targets share (C4 M2L 0.851 -> 0.822
+  // ms; at order 20 the extra barrier and a spill cost more: 0.371 -> 0.420)
+  static constexpr int JH = PM / 2;
+  static constexpr bool HALF_EX = M2L_HALF && M2L_IMM && PM > 20;
+  static constexpr int SMEM_EX = (HALF_EX ? 2 * (JH + 1) : R) * STR * 8;
   // resident warps per SM the register budget allows (128 / 168 / 252 regs)
   static constexpr int WARPS = PM <= 20 ? 16 : (PM <= 24 ? 12 : 8);
   static constexpr int MINB = WARPS / (M2L_ITEM / 32);
@@ -480,10 +490,10 @@ __device__ __forceinline__ void m2l_emit(double2* local, double2* partials,
 
 // exact-order contraction with compile-time (j, k): every output's chain in
 // the order of the table form, coefficients as constant expressions
-template <int PM, int J, int STR>
-__device__ __forceinline__ void m2l_outputs(const double* ax, const double* ay, cplx pw, cplx inv,
+template <int PM, int J, int JE, int JB, int STR>
+__device__ __forceinline__ void m2l_outputs(const double* ax, const double* ay, cplx& pw, cplx inv,
                                             double* red, int tid) {
-  if constexpr (J <= PM) {
+  if constexpr (J <= JE) {
     double sx = ax[0], sy = ay[0];
     m2l_chain<PM, J, 2>(sx, sy, ax, ay);
     cplx b{sx, sy};
@@ -491,9 +501,9 @@ __device__ __forceinline__ void m2l_outputs(const double* ax, const double* ay, 
       b = cmul(b, pw);
       pw = cmul(pw, inv);
     }
-    red[(2 * J) * STR + tid] = b.x;
-    red[(2 * J + 1) * STR + tid] = b.y;
-    m2l_outputs<PM, J + 1, STR>(ax, ay, pw, inv, red, tid);
+    red[(2 * (J - JB)) * STR + tid] = b.x;
+    red[(2 * (J - JB) + 1) * STR + tid] = b.y;
+    m2l_outputs<PM, J + 1, JE, JB, STR>(ax, ay, pw, inv, red, tid);
   }
 }
 
@@ -605,9 +615,11 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
       }
     }
     // c_j = sum_k C(j+k-1, k-1) alpha_k ; b_j = c_j / rho^j = c_j inv^j
+    cplx pw_ex = inv;
+    constexpr bool HALF = EX && Cfg::HALF_EX;
 #if M2L_IMM
     if constexpr (EX) {
-      m2l_outputs<PM, 0, Cfg::STR>(ax, ay, inv, inv, red, tid);
+      m2l_outputs<PM, 0, HALF ? Cfg::JH : PM, 0, Cfg::STR>(ax, ay, pw_ex, inv, red, tid);
     } else
 #endif
     {
@@ -649,36 +661,51 @@ k_m2l_dense(const int* __restrict__ lo_ptr, const int* __restrict__ total_ptr,
     }
     __syncthreads();
     const int nseg = s_nseg;
-    const int R = 2 * (p + 1);
     const bool first_cont = it > 0 && prev_t == s_t[0];
     const int nvalid = s_seg[nseg];
     const bool last_cont = nvalid == M2L_ITEM && next_t >= 0 && next_t == s_t[nvalid - 1];
-    for (int task = tid; task < nseg * R; task += M2L_ITEM) {
-      const int sg = task / R, r = task - sg * R;
-      const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
-      const double* row = red + r * Cfg::STR;
-      // an in-place target's old value is fetched before the sum (its global
-      // round trip overlaps the SMEM reads)
-      const bool sb = sg == 0 && first_cont, ea = sg == nseg - 1 && last_cont;
-      double* dst = reinterpret_cast<double*>(local + (long long)s_t[q0] * (p + 1)) + r;
-      const double old = (!sb && !ea) ? *dst : 0.0;
-      // four interleaved chains (fixed order), then ((0+1)+(2+3))
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int q = q0;
-      for (; q + 4 <= q1; q += 4) {
-        a0 += row[q];
-        a1 += row[q + 1];
-        a2 += row[q + 2];
-        a3 += row[q + 3];
+    // fold rows [r0, r1) of every segment; SMEM row r - r0 holds row r
+    auto fold = [&](int r0, int r1) {
+      const int R = r1 - r0;
+      for (int task = tid; task < nseg * R; task += M2L_ITEM) {
+        const int sg = task / R, rr = task - sg * R, r = r0 + rr;
+        const int q0 = s_seg[sg], q1 = s_seg[sg + 1];
+        const double* row = red + rr * Cfg::STR;
+        // an in-place target's old value is fetched before the sum (its global
+        // round trip overlaps the SMEM reads)
+        const bool sb = sg == 0 && first_cont, ea = sg == nseg - 1 && last_cont;
+        double* dst = reinterpret_cast<double*>(local + (long long)s_t[q0] * (p + 1)) + r;
+        const double old = (!sb && !ea) ? *dst : 0.0;
+        // four interleaved chains (fixed order), then ((0+1)+(2+3))
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int q = q0;
+        for (; q + 4 <= q1; q += 4) {
+          a0 += row[q];
+          a1 += row[q + 1];
+          a2 += row[q + 2];
+          a3 += row[q + 3];
+        }
+        if (q < q1) a0 += row[q];
+        if (q + 1 < q1) a1 += row[q + 1];
+        if (q + 2 < q1) a2 += row[q + 2];
+        const double v = (a0 + a1) + (a2 + a3);
+        if (!sb && !ea)
+          *dst = old + v;
+        else
+          m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, v, sb, ea,
+                   false);
       }
-      if (q < q1) a0 += row[q];
-      if (q + 1 < q1) a1 += row[q + 1];
-      if (q + 2 < q1) a2 += row[q + 2];
-      const double v = (a0 + a1) + (a2 + a3);
-      if (!sb && !ea)
-        *dst = old + v;
-      else
-        m2l_emit(local, partials, item_flags, item, p, s_t[q0], r >> 1, r & 1, v, sb, ea, false);
+    };
+    if constexpr (HALF) {
+      fold(0, 2 * (Cfg::JH + 1));
+      __syncthreads();
+#if M2L_IMM
+      m2l_outputs<PM, Cfg::JH + 1, PM, Cfg::JH + 1, Cfg::STR>(ax, ay, pw_ex, inv, red, tid);
+#endif
+      __syncthreads();
+      fold(2 * (Cfg::JH + 1), 2 * (p + 1));
+    } else {
+      fold(0, 2 * (p + 1));
     }
     // the item's chain flags as one byte store (no memset, no atomics): 1 head
     // part in slot 0, 2 tail part in slot 1, 5 the whole item continues a chain
@@ -1175,11 +1202,12 @@ struct Launch {
         static unsigned attr_dense[2] = {0, 0};
         const bool ex = E.p == PM;
         auto kern = ex ? k_m2l_dense<PM, true> : k_m2l_dense<PM, false>;
-        ensure_smem_attr(kern, Cfg::SMEM, attr_dense[ex]);
+        const int smem = ex ? Cfg::SMEM_EX : Cfg::SMEM;
+        ensure_smem_attr(kern, smem, attr_dense[ex]);
         const unsigned grid = (unsigned)std::min<long long>(
             std::max(1ll, items), (long long)M2L_GRID_WAVES * Cfg::MINB * sm_count());
         note_launch();
-        launch(kern, grid, M2L_ITEM, Cfg::SMEM, st,
+        launch(kern, grid, M2L_ITEM, smem, st,
             lo, total, Ls.weak_idx.as<int>(), Ls.weak_tgt.as<int>(), T.box_cx.as<double>(),
             T.box_cy.as<double>(), E.mult.as<double2>(), E.local.as<double2>(),
             E.partials.as<double2>(), E.item_flags.as<unsigned char>(), E.p, dstat);
