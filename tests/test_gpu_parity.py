@@ -105,6 +105,8 @@ CASES = [
     # (> 32 points per leaf, several 64-point passes), uniform and clustered
     ("uniform", 4_000, 14, 30_000, False, F.TreeConfig(35, 0.5, 17)),
     ("uniform", 4_000, 15, 30_000, True, F.TreeConfig(35, 0.5, 17)),
+    # exact-order M2L with the two-phase fold at the largest dense order
+    ("normal", 8_000, 16, None, False, F.TreeConfig(35, 0.5, 32)),
 ]
 
 
