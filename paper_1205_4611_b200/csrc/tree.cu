@@ -28,6 +28,9 @@ namespace fmm {
 namespace {
 
 constexpr int PART_THREADS = 256;
+#ifndef TREE_SUB_PIPE
+#define TREE_SUB_PIPE 1   // subtree step tables finished after the partition passes
+#endif
 #ifndef TREE_PART_ITEMS
 #define TREE_PART_ITEMS 4
 #endif
@@ -460,7 +463,12 @@ k_subtree(SubArgs A, DevStatus* st) {
   const int n = off_sb[j0 + 1] - g0;
   const int nmax = A.nmax;
   const int nseg_max = 1 << (A.S - A.sb);
+#if TREE_SUB_PIPE
+  Rect* s_rect = reinterpret_cast<Rect*>(smem_raw);       // this CTA's segment rectangles
+  int2* sx = reinterpret_cast<int2*>(s_rect + nseg_max);
+#else
   int2* sx = reinterpret_cast<int2*>(smem_raw);
+#endif
   int2* sy = sx + nmax;
   int2* scr = sy + nmax;
   unsigned short* segid = reinterpret_cast<unsigned short*>(scr + nmax);
@@ -496,6 +504,43 @@ k_subtree(SubArgs A, DevStatus* st) {
   for (int s = A.sb; s < A.S; ++s) {
     const int nloc = 1 << (s - A.sb);
     const int* off = A.a.off + off_base(s);
+#if TREE_SUB_PIPE
+    // segment q = threadIdx.x (nloc <= SUB_THREADS, checked by the host):
+    // the axis comes from the rectangle this CTA computed one step earlier
+    // (SMEM) and the cut rank from the SMEM records, so the partition starts
+    // after one round trip (the rank -> original index lookups); the
+    // coordinate loads behind them land during the two partition passes and
+    // the step tables are finished after them (prepare_segment's work, split)
+    const int q = threadIdx.x;
+    const bool qa = q < nloc;
+    const long long j = j0 * nloc + q;
+    int s0 = 0, nn = 0, k = 0;
+    Rect r{0.0, 0.0, 0.0, 0.0};
+    bool along_y = false;
+    double2 pc{}, pn{}, pxa{}, pxb{}, pya{}, pyb{};
+    if (qa) {
+      s0 = off[j] - g0;
+      nn = off[j + 1] - off[j];
+      k = (nn + 1) / 2;
+      r = s == A.sb ? A.a.rect_tab[step_base(s) + j] : s_rect[q];
+      along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
+      const int kn = k < nn ? k : k - 1;
+      const int ik = along_y ? A.a.perm_y[sy[s0 + k - 1].y] : A.a.perm_x[sx[s0 + k - 1].x];
+      const int in = along_y ? A.a.perm_y[sy[s0 + kn].y] : A.a.perm_x[sx[s0 + kn].x];
+      const int ixa = A.a.perm_x[sx[s0].x], ixb = A.a.perm_x[sx[s0 + nn - 1].x];
+      const int iya = A.a.perm_y[sy[s0].y], iyb = A.a.perm_y[sy[s0 + nn - 1].y];
+      pc = A.a.pos[ik];
+      pn = A.a.pos[in];
+      pxa = A.a.pos[ixa];
+      pxb = A.a.pos[ixb];
+      pya = A.a.pos[iya];
+      pyb = A.a.pos[iyb];
+      q_s0[q] = s0;
+      q_k[q] = k;
+      q_cr[q] = along_y ? sy[s0 + k - 1].y : sx[s0 + k - 1].x;
+      q_ax[q] = along_y;
+    }
+#else
     for (int q = threadIdx.x; q < nloc; q += blockDim.x) {
       const long long j = j0 * nloc + q;
       const int s0 = off[j] - g0, nn = off[j + 1] - off[j], k = (nn + 1) / 2;
@@ -510,6 +555,7 @@ k_subtree(SubArgs A, DevStatus* st) {
       q_cr[q] = cr;
       q_ax[q] = along_y;
     }
+#endif
     __syncthreads();
     // pass 1: flags of the moving copy; record the in-warp prefix at segment starts
     int run = 0;
@@ -569,6 +615,28 @@ k_subtree(SubArgs A, DevStatus* st) {
       if (q_ax[q]) sx[i] = scr[i]; else sy[i] = scr[i];
       segid[i] = (unsigned short)(2 * q + (i - q_s0[q] >= q_k[q]));
     }
+#if TREE_SUB_PIPE
+    if (qa) {   // the step tables (prepare_segment's second wave, same values)
+      const int sg = s + A.a.s0;                                   // global step
+      const bool deg = (sg & 1) == 0 && (sg >> 1) < A.a.L;         // tree.py:285
+      const double cut = along_y ? pc.y : pc.x;
+      if (deg && pxa.x == pxb.x && pya.y == pyb.y) {
+        const unsigned long long key = ((unsigned long long)(sg >> 1) << 40) |
+                                       (unsigned long long)((A.a.seg << s) + j);
+        atomicMin(&st->degenerate_key, key);
+        atomicOr(&st->flags, ST_DEGENERATE);
+      }
+      if (k < nn && (along_y ? pn.y : pn.x) == cut) atomicOr(&st->flags, ST_EVAL_TIES);
+      A.a.cut_tab[step_base(s) + j] = cut;
+      A.a.axis_tab[step_base(s) + j] = along_y;
+      Rect lo = r, hi = r;                                         // tree.py:218-222
+      if (along_y) { lo.y1 = cut; hi.y0 = cut; } else { lo.x1 = cut; hi.x0 = cut; }
+      A.a.rect_tab[step_base(s + 1) + 2 * j] = lo;
+      A.a.rect_tab[step_base(s + 1) + 2 * j + 1] = hi;
+      s_rect[2 * q] = lo;
+      s_rect[2 * q + 1] = hi;
+    }
+#endif
     __syncthreads();
   }
 
@@ -713,7 +781,8 @@ void radix_sort_pairs(DBuf& tmp, const K* kin, K* kout, const V* vin, V* vout, l
 }
 
 int smem_need(long long nmax, int nseg) {
-  return (int)(3 * 8 * nmax + 2 * ((nmax + 1) & ~1ll) + 18ll * nseg + 64);
+  return (int)((TREE_SUB_PIPE ? (long long)sizeof(Rect) * nseg : 0) + 3 * 8 * nmax +
+               2 * ((nmax + 1) & ~1ll) + 18ll * nseg + 64);
 }
 
 }  // namespace
@@ -734,12 +803,22 @@ void plan_tree(TreePlan& P, int64_t n, int64_t m, int L, int s0) {
   auto nmax_at = [&](int s) { return (n + (int64_t(1) << s) - 1) >> s; };
   int sb = S;
   bool fits_any = false;
+  // the pipelined subtree step gives each segment of a step its own thread
+  auto seg_ok = [&](int s) { return !TREE_SUB_PIPE || (1ll << (S - s)) <= SUB_THREADS; };
   for (int s = 0; s <= S; ++s) {
-    if (smem_need(nmax_at(s), 1 << (S - s)) <= SMEM_BUDGET) { sb = s; fits_any = true; break; }
+    if (seg_ok(s) && smem_need(nmax_at(s), 1 << (S - s)) <= SMEM_BUDGET) {
+      sb = s;
+      fits_any = true;
+      break;
+    }
   }
   if (!fits_any) {
     for (int s = 0; s <= S; ++s)
-      if (smem_need(nmax_at(s), 1 << (S - s)) <= 220 * 1024) { sb = s; fits_any = true; break; }
+      if (seg_ok(s) && smem_need(nmax_at(s), 1 << (S - s)) <= 220 * 1024) {
+        sb = s;
+        fits_any = true;
+        break;
+      }
   }
   const int64_t leaf_max = nmax_at(S);
   P.global_leaf_finalize = !fits_any || leaf_max > LEAF_SMEM_MAX;
