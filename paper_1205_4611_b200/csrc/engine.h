@@ -50,6 +50,10 @@ struct TreePlan {
   std::vector<int> tile_count;       // per global step
   DBuf d_off;                        // int32 offsets for steps 0..S (+1 per step)
   DBuf d_tile_seg, d_tile_start;     // concatenated tile tables of all global steps
+  DBuf d_tile_desc;                  // per tile: {segment, tile start, segment start, end}
+  std::vector<int> segt_base;        // per step: base of its first-tile-per-segment table
+  DBuf d_seg_tile0;                  // per step and segment: first tile (+ sentinel)
+  DBuf d_tile_flag;                  // per tile: parities + axis, written by the step before
 };
 
 __host__ __device__ inline int64_t step_base(int s) { return (int64_t(1) << s) - 1; }          // per-segment tables

@@ -28,6 +28,9 @@ namespace fmm {
 namespace {
 
 constexpr int PART_THREADS = 256;
+#ifndef TREE_PART_DESC
+#define TREE_PART_DESC 1   // split steps read a per-tile descriptor + flag byte
+#endif
 #ifndef TREE_SUB_PIPE
 #define TREE_SUB_PIPE 1   // subtree step tables finished after the partition passes
 #endif
@@ -337,6 +340,17 @@ __device__ __forceinline__ void prepare_segment(const StepArgs& a, int s, long l
   (void)s0;
 }
 
+// per-tile descriptors of a split step (TREE_PART_DESC): static {segment,
+// tile start, segment start, end}, the flag bytes of this step (null: the
+// first step, read the segment tables) and of the next (null: the subtree
+// kernel takes over), and the next step's first tile per segment
+struct PartDesc {
+  const int* desc;
+  const unsigned char* flag_in;
+  unsigned char* flag_out;
+  const int* segt_next;
+};
+
 // stable partition of the moving copy, tiles aligned to segments
 __device__ __forceinline__ bool part_flag(int2 e, bool along_y, int cr) {
   return (along_y ? e.y : e.x) <= cr;
@@ -352,7 +366,8 @@ __global__ void __launch_bounds__(PART_THREADS)
 k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
             const int* __restrict__ tile_start, int2* X0, int2* X1, int2* Y0, int2* Y1,
             const unsigned char* xpar, const unsigned char* ypar, unsigned char* xpar_next,
-            unsigned char* ypar_next, LookbackPacked lbs, unsigned ntiles, DevStatus* st) {
+            unsigned char* ypar_next, LookbackPacked lbs, unsigned ntiles, DevStatus* st,
+            PartDesc pd) {
   pdl_enter();
   __shared__ unsigned s_tile;
   __shared__ int sw[PART_THREADS / 32];
@@ -360,6 +375,29 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
   if (threadIdx.x == 0) s_tile = lb_ticket(lbs, ntiles);
   __syncthreads();
   const unsigned t = s_tile;
+#if TREE_PART_DESC
+  // one round trip for everything the partition needs: the static tile
+  // descriptor and the flag byte the previous step's head tile wrote
+  // (parities and axis); only the first step reads the segment tables
+  const int4 td = reinterpret_cast<const int4*>(pd.desc)[t];
+  const unsigned fl = pd.flag_in ? pd.flag_in[t] : 0u;
+  const int j = td.x, tstart = td.y, s0 = td.z, end = td.w, n = end - s0, k = (n + 1) / 2;
+  unsigned char xp, yp;
+  bool along_y;
+  if (pd.flag_in) {
+    xp = fl & 1u;
+    yp = (fl >> 1) & 1u;
+    along_y = (fl >> 2) & 1u;
+  } else {
+    xp = xpar[j];
+    yp = ypar[j];
+    const Rect r = a.rect_tab[step_base(s) + j];
+    along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;              // geometry.py:63
+  }
+  const int2* X = xp ? X1 : X0;
+  const int2* Y = yp ? Y1 : Y0;
+  const bool head = tstart == s0;
+#else
   const int j = tile_seg[t];
   const int* off = a.off + off_base(s);
   const int s0 = off[j], end = off[j + 1], n = end - s0, k = (n + 1) / 2;
@@ -370,6 +408,7 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
   const bool head = tstart == s0;
   const Rect r = a.rect_tab[step_base(s) + j];
   const bool along_y = (r.y1 - r.y0) / 2 > (r.x1 - r.x0) / 2;      // geometry.py:63
+#endif
   const int cr = along_y ? Y[s0 + k - 1].y : X[s0 + k - 1].x;
   const int2* M = along_y ? X : Y;
   int2* D = along_y ? (xp ? X0 : X1) : (yp ? Y0 : Y1);
@@ -430,6 +469,21 @@ k_part_step(StepArgs a, int s, const int* __restrict__ tile_seg,
     const unsigned char nyp = along_y ? yp : (unsigned char)(1 - yp);
     xpar_next[2 * j] = nxp; xpar_next[2 * j + 1] = nxp;
     ypar_next[2 * j] = nyp; ypar_next[2 * j + 1] = nyp;
+#if TREE_PART_DESC
+    if (pd.flag_out) {
+      // children's flag bytes, one per tile of the next step (axis from the
+      // child rectangles prepare_segment just wrote)
+      const Rect lo = a.rect_tab[step_base(s + 1) + 2 * j];
+      const Rect hi = a.rect_tab[step_base(s + 1) + 2 * j + 1];
+      const unsigned base = nxp | (nyp << 1);
+      const unsigned f0 = base | (((lo.y1 - lo.y0) / 2 > (lo.x1 - lo.x0) / 2) ? 4u : 0u);
+      const unsigned f1 = base | (((hi.y1 - hi.y0) / 2 > (hi.x1 - hi.x0) / 2) ? 4u : 0u);
+      const int c0 = pd.segt_next[2 * j], c1 = pd.segt_next[2 * j + 1],
+                c2 = pd.segt_next[2 * j + 2];
+      for (int q = c0; q < c1; ++q) pd.flag_out[q] = (unsigned char)f0;
+      for (int q = c1; q < c2; ++q) pd.flag_out[q] = (unsigned char)f1;
+    }
+#endif
   }
 }
 
@@ -862,6 +916,35 @@ void plan_tree(TreePlan& P, int64_t n, int64_t m, int L, int s0) {
     FMM_CUDA(cudaMemcpy(P.d_off.p, flat.data(), sizeof(int) * off_entries,
                         cudaMemcpyHostToDevice));
   }
+  {
+    // per-tile descriptors, first tile of every segment per step, flag bytes
+    std::vector<int> desc(4 * tseg.size() + 4), st0;
+    P.segt_base.assign(sb + 1, 0);
+    for (int s = 0; s < sb; ++s) {
+      P.segt_base[s] = (int)st0.size();
+      const int tb = P.tile_base[s];
+      int t = 0;
+      for (size_t j = 0; j + 1 < off[s].size(); ++j) {
+        st0.push_back(t);
+        for (int64_t b = off[s][j]; b < off[s][j + 1]; b += PART_TILE, ++t) {
+          desc[4 * (tb + t)] = (int)j;
+          desc[4 * (tb + t) + 1] = (int)b;
+          desc[4 * (tb + t) + 2] = (int)off[s][j];
+          desc[4 * (tb + t) + 3] = (int)off[s][j + 1];
+        }
+      }
+      st0.push_back(t);
+    }
+    P.segt_base[sb] = (int)st0.size();
+    st0.push_back(0);
+    P.d_tile_desc.reserve(sizeof(int) * desc.size());
+    P.d_seg_tile0.reserve(sizeof(int) * st0.size());
+    P.d_tile_flag.reserve(tseg.size() + 16);
+    FMM_CUDA(cudaMemcpy(P.d_tile_desc.p, desc.data(), sizeof(int) * desc.size(),
+                        cudaMemcpyHostToDevice));
+    FMM_CUDA(cudaMemcpy(P.d_seg_tile0.p, st0.data(), sizeof(int) * st0.size(),
+                        cudaMemcpyHostToDevice));
+  }
   P.d_tile_seg.reserve(sizeof(int) * (tseg.size() + 1));
   P.d_tile_start.reserve(sizeof(int) * (tstart.size() + 1));
   if (!tseg.empty()) {
@@ -1018,9 +1101,14 @@ void run_tree(TreeState& T, TreePlan& P, DevStatus* dstat, cudaStream_t st) {
       const LookbackPacked lbs{T.lb_vals.as<unsigned long long>(), T.lb_ticket.as<unsigned>(),
                                T.lb_epoch, T.lb_base.as<unsigned>()};
       note_launch();
+      unsigned char* flags = P.d_tile_flag.as<unsigned char>();
+      const PartDesc pd{P.d_tile_desc.as<int>() + 4ll * P.tile_base[s],
+                        s > 0 ? flags + P.tile_base[s] : nullptr,
+                        s + 1 < sb ? flags + P.tile_base[s + 1] : nullptr,
+                        s + 1 < sb ? P.d_seg_tile0.as<int>() + P.segt_base[s + 1] : nullptr};
       launch(k_part_step, nt, PART_THREADS, 0, st, a, s, tseg, tstart, T.X0.as<int2>(),
                                                T.X1.as<int2>(), T.Y0.as<int2>(), T.Y1.as<int2>(),
-                                               xp, yp, xq, yq, lbs, (unsigned)nt, dstat);
+                                               xp, yp, xq, yq, lbs, (unsigned)nt, dstat, pd);
       std::swap(xp, xq);
       std::swap(yp, yq);
     }
